@@ -1,0 +1,385 @@
+"""Benchmark of the batched XFT fast LCT (BASELINE.json metric).
+
+Default workload = BASELINE config 2: 4096 rows x N=4096, per-row FrFT angle
+alpha ~ U(0, pi) (seed 1), rows i.i.d. CN(0,1); one step = the whole batch
+transformed in complex64 AND in complex128 (metric "batched LCT Msamples/s at
+N=4096 c64/c128").  `value` is whole-job throughput with inputs resident in
+HBM (CUDA events on the launching stream, max over ranks); `e2e` is the same
+metric through the public host-buffer API (ops.lct_host -> xft_lct_host:
+pinned host in, H2D + kernel + D2H, host out).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg4|...]
+  python bench.py --impl reference ...   # CPU reference path (oracle port), rank 0 only
+
+Multi-GPU (torchrun): rows are independent, so every rank transforms its own
+full batch with no collective (weak scaling); value = N x per-rank samples /
+max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML poller)
+# ---------------------------------------------------------------------------
+_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self.period = period_s
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+
+    def summary(self):
+        if self._nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        names = [v for k, v in _REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def make_workload(name: str, rows_override=None):
+    from paper_0912_1379_b200 import workloads as W
+
+    if name == "cfg2":
+        rows = rows_override or 4096
+        c64 = W.config2(rows=rows, n=4096, dtype=np.complex64)
+        c128 = W.config2(rows=rows, n=4096, dtype=np.complex128)
+        return [("c64", c64.values, c64.abcd), ("c128", c128.values, c128.abcd)], \
+            {"workload": f"cfg2 batched FrFT {rows}x4096 c64+c128, per-row alpha~U(0,pi) seed 1",
+             "rows": rows, "n": 4096}
+    if name == "cfg4":
+        c4 = W.config4(rows=rows_override or 65536)
+        return [("c64", c4.values, c4.abcd)], \
+            {"workload": f"cfg4 Fourier (0,1,-1,0) {c4.values.shape[0]}x1024 c64, Hermite mixtures seed 3",
+             "rows": c4.values.shape[0], "n": 1024}
+    if name == "cfg1":
+        c1 = W.config1()
+        return [("c128", c1.values, c1.abcd)], {"workload": "cfg1 single LCT 1x1024 c128 (2,1,1,1)", "rows": 1, "n": 1024}
+    raise SystemExit(f"unknown config {name}")
+
+
+def samples_of(work):
+    return sum(v.shape[0] * v.shape[1] for _, v, _ in work)
+
+
+def bytes_of(work):
+    return sum(v.nbytes * 2 for _, v, _ in work)  # read + write of every sample
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port) timing
+# ---------------------------------------------------------------------------
+def _cpu_worker(args):
+    abcd, vals = args
+    from oracle import xft_oracle
+
+    t0 = time.perf_counter()
+    xft_oracle.fast_lct_rows(abcd, vals.astype(np.complex128))
+    return time.perf_counter() - t0
+
+
+def cpu_reference(work, sample_rows: int, procs: int, pool=None):
+    """Oracle port of the reference fast_lct over a bounded row sample, process pool of `procs`."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    tasks = []
+    total = 0
+    for _, v, p in work:
+        rows = min(sample_rows, v.shape[0])
+        pr = p if p.ndim == 1 else p[:rows]
+        block = max(1, rows // (procs * 4))
+        for s in range(0, rows, block):
+            e = min(rows, s + block)
+            tasks.append((pr if pr.ndim == 1 else pr[s:e], v[s:e]))
+        total += rows * v.shape[1]
+    ex = pool if pool is not None else ProcessPoolExecutor(procs)
+    try:
+        if pool is None:
+            list(ex.map(_cpu_worker, tasks[:procs]))  # warm the workers (imports)
+        t0 = time.perf_counter()
+        list(ex.map(_cpu_worker, tasks))
+        dt = time.perf_counter() - t0
+    finally:
+        if pool is None:
+            ex.shutdown()
+    return total / dt / 1e6, total, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    work, cfg = make_workload(args.config, args.rows)
+    from concurrent.futures import ProcessPoolExecutor
+
+    procs = len(os.sched_getaffinity(0))
+    # bounded per-step sample so the whole --steps run stays within a few minutes
+    sample_rows = max(procs, min(args.cpu_rows, 32768 // max(1, args.steps)))
+    vals = []
+    with ProcessPoolExecutor(procs) as pool:
+        for _ in range(max(1, args.warmup)):
+            cpu_reference(work, procs, procs, pool)
+        for _ in range(args.steps):
+            v, total, dt = cpu_reference(work, sample_rows, procs, pool)
+            vals.append(v)
+    value = statistics.median(vals)
+    sample = f"{sample_rows} rows per dtype of {cfg['workload']} ({total} samples/step)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Msamples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded)",
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "Msamples/s", "cores": procs, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "Msamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "batched LCT Msamples/s at N=4096 c64/c128"
+
+
+def DTYPE_OF(work):
+    return "+".join(sorted({"c64" if v.dtype == np.complex64 else "c128" for _, v, _ in work}))
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_0912_1379_b200 import ops
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    work, cfg = make_workload(args.config, args.rows)
+    nsets = 3  # rotate 3 input/output sets: every kernel reads cold data
+    sets = []
+    for _ in range(nsets):
+        s = []
+        for tag, v, p in work:
+            vin = torch.from_numpy(v).to(dev)
+            s.append((tag, vin, torch.empty_like(vin), torch.from_numpy(np.ascontiguousarray(p)).to(dev)))
+        sets.append(s)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i, evs=None):
+        for k, (tag, vin, vout, p) in enumerate(sets[i % nsets]):
+            if evs is not None:
+                evs[k][0].record(stream)
+            ops.lct_rows(vin, p, out=vout, validate=False)
+            if evs is not None:
+                evs[k][1].record(stream)
+
+    # validate once (reference order) outside the timed region
+    for _, v, p in work:
+        ops.validate_abcd_host(p)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # per-kernel timing pass (events around every launch)
+    kev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+            for _ in work] for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        step(i, kev[i])
+    torch.cuda.synchronize()
+    kern_ms = [sum(kev[i][k][0].elapsed_time(kev[i][k][1]) for i in range(args.steps)) / args.steps
+               for k in range(len(work))]
+
+    # main timed region: K steps bracketed by barrier + synchronize
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    total_ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    samples = samples_of(work)
+    value = world * samples / (ms_per_step * 1e-3) / 1e6
+
+    # end-to-end through the public host-buffer API
+    e2e_steps = max(2, min(args.steps, args.e2e_steps))
+    pinned = []
+    for tag, v, p in work:
+        hin = torch.from_numpy(v).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        pinned.append((hin.numpy(), hout.numpy(), p))
+    for hin, hout, p in pinned:
+        ops.lct_host(hin, p, out=hout)
+    barrier()
+    te = time.perf_counter()
+    for _ in range(e2e_steps):
+        for hin, hout, p in pinned:
+            ops.lct_host(hin, p, out=hout)
+    e2e_dt = time.perf_counter() - te
+    if world > 1:
+        t = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_dt = float(t.item())
+    e2e_value = world * samples * e2e_steps / e2e_dt / 1e6
+    h2d = sum(h.nbytes + p.nbytes for h, _, p in pinned)
+    d2h = sum(o.nbytes for _, o, _ in pinned)
+
+    if rank != 0:
+        return
+    peak, peak_kind = load_peaks()
+    traffic = load_traffic()
+    per = {}
+    for k, (tag, v, p) in enumerate(work):
+        alg_bytes = v.nbytes * 2
+        ach = alg_bytes / (kern_ms[k] * 1e-3) / 1e9
+        per[tag] = {"kernel_ms": kern_ms[k], "Msamples_per_s": v.size / (kern_ms[k] * 1e-3) / 1e6,
+                    "achieved_GBps": ach, "frac": ach / peak, "alg_bytes_per_launch": alg_bytes,
+                    "traffic": traffic.get(f"{args.config}_{tag}")}
+    dom = max(per, key=lambda t: per[t]["kernel_ms"])
+    roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
+            "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"xft_rows_kernel {dom}",
+            "peak_source": peak_kind,
+            "step_achieved": bytes_of(work) / (ms_per_step * 1e-3) / 1e9}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        procs = len(os.sched_getaffinity(0))
+        v, total, dt = cpu_reference(work, args.cpu_rows, procs)
+        cpu = {"value": v, "unit": "Msamples/s", "cores": procs, "kind": "port",
+               "sample": f"{args.cpu_rows} rows per dtype of the same batch ({total} samples, {dt:.1f} s), "
+                         f"oracle/xft_oracle.py fast_lct_rows in a {procs}-process pool"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "Msamples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded, BASELINE config draw order)",
+        "config": dict(cfg, l2="3 rotating input/output sets; each launch streams >= 2x L2 of cold data",
+                       parallelism=f"batch-sharded x{world}, no collective"),
+        "roofline": roof, "per_dtype": per, "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "Msamples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "api": "paper_0912_1379_b200.ops.lct_host -> xft_lct_host"},
+        "gpu_launches": len(work) * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--rows", type=int, default=None)
+    ap.add_argument("--cpu-rows", type=int, default=512)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,131 @@
+/* xft_b200.h -- C ABI of the B200-native XFT fast linear canonical transform.
+ *
+ * Drop-in boundary for the reference's hot path (reference = the pure-Python
+ * `xft` package, /root/reference/pkg/src/xft).  Every entry point takes plain
+ * pointers and sizes; no torch / CUDA C++ types cross the boundary (streams
+ * are passed as `void*` = cudaStream_t, NULL = legacy default stream).
+ *
+ * Conventions (all fixed by the reference):
+ *   grid      x_k = (2k - n + 1) * pi / (2 sqrt(2n))          xft/hermite.py:80-89
+ *   DFT       out[j] = sum_k e^{sign 2 pi i jk/n} in[k]        xft/fftcore.py:1-8
+ *   LCT       out[j] = C(n) p_j e^{i psi_j}/sqrt(2 pi i b) DFT(p_k e^{i phi_k} in[k])[j]
+ *             with DFT_SIGN = -1                                xft/lct.py:168-208
+ *   output nodes y_j = 4 b x_j / pi (not materialised; see xft_output_nodes)
+ *
+ * Layout: `batch` contiguous rows of `n` complex samples, interleaved
+ * (re, im) pairs -- complex64 = 2 x float32, complex128 = 2 x float64 --
+ * i.e. the memory layout of numpy/torch complex arrays.  Out-of-place; the
+ * input is never written (reference contract xft/fftcore.py:113).
+ *
+ * Status codes mirror the reference exception classes (xft/errors.py:4-49).
+ * Device entry points are stream-ordered and never synchronise the host;
+ * parameters passed through device memory are assumed pre-validated (call
+ * xft_validate_lct_params on the host copy, as the Python layer does).
+ * All entry points are thread-safe; the only global state is the lazily
+ * built, immutable per-(device, n, dtype) twiddle/phase tables.
+ */
+#ifndef XFT_B200_H
+#define XFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference exception class in brackets) ---------------- */
+#define XFT_OK 0
+#define XFT_EINVALID_SIZE 1  /* [InvalidSizeError]        xft/errors.py:8   */
+#define XFT_EPARAM 2         /* [ParameterError]          xft/errors.py:12  */
+#define XFT_ESINGULAR 3      /* [SingularParameterError]  xft/errors.py:16  */
+#define XFT_EDEGENERATE 4    /* [DegenerateParameterError] xft/errors.py:20 */
+#define XFT_EBRANCH 5        /* [UnsupportedBranchError]  xft/errors.py:25  */
+#define XFT_ESHAPE 6         /* [ShapeError]              xft/errors.py:29  */
+#define XFT_EGRID 7          /* [GridMismatchError]       xft/errors.py:33  */
+#define XFT_ECUDA 8          /* CUDA runtime failure (no reference analogue) */
+#define XFT_ENOTSUP 9        /* size/dtype combination not built           */
+
+/* ---- element types ----------------------------------------------------------- */
+#define XFT_C64 0   /* complex64: float32 (re, im)  */
+#define XFT_C128 1  /* complex128: float64 (re, im) */
+
+/* ---- flags --------------------------------------------------------------------- */
+#define XFT_FLAG_BARE_FOURIER 1 /* multiply by sqrt(2 pi i): xft_fourier, xft/lct.py:211-223 */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int xft_version(void);
+
+/* Largest power-of-two row length the single-kernel path accepts for dtype. */
+int64_t xft_max_n(int dtype);
+
+/* Build (once) the immutable tables for (current device, n, dtype).  Must be
+ * called outside CUDA-graph capture; the transform entry points call it
+ * lazily otherwise.  Replaces the plan construction of DftPlan.__init__ /
+ * plan_dft (xft/fftcore.py:73-105). */
+int xft_prepare(int64_t n, int dtype);
+
+/* Host-side validation of LCT parameters in the reference's order:
+ *   b == 0                        -> XFT_EDEGENERATE   (xft/lct.py:187-190)
+ *   |ad - bc - 1| > tol (check=1) -> XFT_EPARAM        (xft/lct.py:191-192, 66-71)
+ * abcd: host array of `count` rows of 4 doubles with row stride `stride`
+ * (0 = one quadruple shared by all rows).  On failure *bad_row (if non-NULL)
+ * receives the first offending row. */
+int xft_validate_lct_params(const double* abcd, int64_t count, int64_t stride, int check_unimodular,
+                            double tol, int64_t* bad_row);
+
+/* Batched fast LCT (device pointers).  Replaces fast_lct (xft/lct.py:168-208),
+ * fast_frft (226-233) and, with XFT_FLAG_BARE_FOURIER, xft_fourier (211-223).
+ *   in, out   : device, batch x n complex (dtype)
+ *   abcd      : device, per-row (a,b,c,d) doubles, row stride abcd_stride
+ *               (4 = per-row parameters, 0 = one quadruple for all rows)
+ *   stream    : cudaStream_t */
+int xft_lct(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+            int64_t abcd_stride, int flags, void* stream);
+
+/* Batched unnormalised DFT, sign = +1 or -1 (device pointers).
+ * Replaces apply_dft(plan_dft(n, sign), v) (xft/fftcore.py:103-119). */
+int xft_dft(const void* in, void* out, int64_t batch, int64_t n, int sign, int dtype, void* stream);
+
+/* Batched scaled Fourier kernel F v = C(n) p * DFT(p * v) (device pointers).
+ * Replaces apply_scaled_fourier (xft/kernel.py:83-95). */
+int xft_scaled_fourier(const void* in, void* out, int64_t batch, int64_t n, int dtype, void* stream);
+
+/* End-to-end LCT on HOST buffers: validates abcd (host, reference order),
+ * streams the batch through the device in chunks (H2D / kernel / D2H
+ * overlapped on the library's own streams) and returns when `out` holds
+ * the result.  Pinned host buffers give full link bandwidth; pageable
+ * buffers work but stage through the driver.  The call a reference-side
+ * ctypes/cffi binding makes. */
+int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+                 int64_t abcd_stride, int flags, int check_unimodular, double tol);
+
+/* Complex-z fractional transform through the Mehler kernel (device pointers):
+ *   out_j = dx sqrt(2/(1-z^2)) sum_k exp(-((1+z^2)(x_j^2+x_k^2) - 4 x_j x_k z) / (2(1-z^2))) in_k
+ * i.e. frft_matrix_asymptotic(n, FrftOrder(z)).apply(in) (xft/dense.py:122-151,
+ * 76-80) evaluated in O(n log n) as a Bluestein convolution.  z: device array
+ * of batch (re, im) pairs (z_stride 2) or one pair (z_stride 0); |z| <= 1,
+ * z != +-1 validated by the caller (xft_validate_mehler_z).  dtype C128 only
+ * (the reference tolerance 1e-12 needs fp64).  `workspace` : device scratch of
+ * xft_mehler_workspace_bytes(batch, n) bytes. */
+int64_t xft_mehler_workspace_bytes(int64_t batch, int64_t n);
+int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double* z, int64_t z_stride,
+               void* workspace, void* stream);
+/* Host check of z values (FrftOrder / mehler_kernel, xft/dense.py:49-59, 127-130). */
+int xft_validate_mehler_z(const double* z, int64_t count, int64_t stride, int64_t* bad_row);
+
+/* Separable 2-D LCT on one device: fast LCT along rows (abcd_row) then along
+ * columns (abcd_col) of an n_rows x n_cols field.  `workspace`: device scratch
+ * of n_rows*n_cols complex elements (dtype).  Composition of fast_lct along
+ * axis 1 then axis 0 (no reference symbol; SURVEY 8(a) last row). */
+int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dtype, const double* abcd_row,
+              const double* abcd_col, void* workspace, void* stream);
+
+/* Tiled transpose used by the 2-D pass and the sharded all-to-all layout:
+ * out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols. */
+int xft_transpose(const void* in, void* out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
+                  int dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XFT_B200_H */

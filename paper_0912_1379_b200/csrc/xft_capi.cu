@@ -1,0 +1,302 @@
+// C-ABI entry points (include/xft_b200.h) for the 1-D row transforms,
+// validation, the host end-to-end pipeline, the transpose and the 2-D pass.
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <utility>
+
+#include "../../include/xft_b200.h"
+#include "xft_rows.cuh"
+#include "xft_tables.h"
+
+using namespace xftb;
+
+namespace {
+
+constexpr int MAXLOG_C64 = 14;   // 16384 x 8 B = 128 KiB per row in shared memory
+constexpr int MAXLOG_C128 = 13;  //  8192 x 16 B = 128 KiB
+
+template <class C, int L>
+constexpr int pick_e() {
+  if (L == 0) return 1;
+  if (sizeof(C) == 8) return L >= 4 ? 16 : (1 << L);        // c64: radix-16 passes
+  return L >= 13 ? 16 : (L >= 3 ? 8 : (1 << L));           // c128: radix-8 (16 at 8192)
+}
+
+struct LaunchArgs {
+  const void* in;
+  void* out;
+  long long batch;
+  const double* abcd;
+  long long stride;
+  Abcd uni;
+  Tables tb;
+  int flags;
+  cudaStream_t st;
+};
+
+using LaunchFn = int (*)(const LaunchArgs&);
+
+template <class C, int L, int MODE, int SIGN>
+int launch_rows(const LaunchArgs& a) {
+  using Cfg = RowCfg<C, L, pick_e<C, L>(), MODE, SIGN>;
+  auto kern = xft_rows_kernel<Cfg>;
+  if (Cfg::SMEM > 48 * 1024) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
+      return XFT_ECUDA;
+  }
+  const long long grid = (a.batch + Cfg::ROWS - 1) / Cfg::ROWS;
+  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
+      static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
+      static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.cn, a.tb.half, a.flags);
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+template <class C, int MODE, int SIGN, int... Ls>
+constexpr auto make_table(std::integer_sequence<int, Ls...>) {
+  return std::array<LaunchFn, sizeof...(Ls)>{&launch_rows<C, Ls, MODE, SIGN>...};
+}
+
+template <class C, int MODE, int SIGN, int MAXL>
+LaunchFn pick(int l) {
+  static const auto tab = make_table<C, MODE, SIGN>(std::make_integer_sequence<int, MAXL + 1>{});
+  return (l >= 0 && l <= MAXL) ? tab[l] : nullptr;
+}
+
+int log2_exact(int64_t n) {
+  if (n < 1 || (n & (n - 1))) return -1;
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+
+int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype,
+             const double* abcd, int64_t stride, Abcd uni, int flags, cudaStream_t st) {
+  if (n < 1) return XFT_EINVALID_SIZE;
+  if (batch < 0) return XFT_EINVALID_SIZE;
+  if (dtype != XFT_C64 && dtype != XFT_C128) return XFT_EPARAM;
+  const int l = log2_exact(n);
+  if (l < 0 || l > (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128)) return XFT_ENOTSUP;
+  if (batch == 0) return XFT_OK;
+  LaunchArgs a{in, out, (long long)batch, abcd, (long long)stride, uni, {}, flags, st};
+  int rc = get_tables(n, dtype, &a.tb);
+  if (rc) return rc;
+  LaunchFn fn = nullptr;
+  if (dtype == XFT_C64) {
+    if (mode == MODE_LCT) fn = pick<float2, MODE_LCT, -1, MAXLOG_C64>(l);
+    else if (mode == MODE_SCALED) fn = pick<float2, MODE_SCALED, -1, MAXLOG_C64>(l);
+    else fn = sign < 0 ? pick<float2, MODE_DFT, -1, MAXLOG_C64>(l) : pick<float2, MODE_DFT, 1, MAXLOG_C64>(l);
+  } else {
+    if (mode == MODE_LCT) fn = pick<double2, MODE_LCT, -1, MAXLOG_C128>(l);
+    else if (mode == MODE_SCALED) fn = pick<double2, MODE_SCALED, -1, MAXLOG_C128>(l);
+    else fn = sign < 0 ? pick<double2, MODE_DFT, -1, MAXLOG_C128>(l) : pick<double2, MODE_DFT, 1, MAXLOG_C128>(l);
+  }
+  if (!fn) return XFT_ENOTSUP;
+  return fn(a);
+}
+
+// ---------------------------------------------------------------------------
+// tiled transpose: out[c * ld_out + r] = in[r * ld_in + c]
+// ---------------------------------------------------------------------------
+template <class C, int TILE>
+__global__ void __launch_bounds__(TILE * 8) transpose_kernel(const C* __restrict__ in, C* __restrict__ out,
+                                                           long long rows, long long cols, long long ld_in,
+                                                           long long ld_out) {
+  __shared__ C tile[TILE][TILE + 1];
+  const long long r0 = (long long)blockIdx.y * TILE, c0 = (long long)blockIdx.x * TILE;
+  const int tx = threadIdx.x % TILE, ty = threadIdx.x / TILE;
+#pragma unroll
+  for (int k = ty; k < TILE; k += 8) {
+    const long long r = r0 + k, c = c0 + tx;
+    if (r < rows && c < cols) tile[k][tx] = in[r * ld_in + c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = ty; k < TILE; k += 8) {
+    const long long c = c0 + k, r = r0 + tx;
+    if (r < rows && c < cols) out[c * ld_out + r] = tile[tx][k];
+  }
+}
+
+template <class C>
+int launch_transpose(const void* in, void* out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,
+                     cudaStream_t st) {
+  constexpr int TILE = 32;
+  dim3 grid((unsigned)((cols + TILE - 1) / TILE), (unsigned)((rows + TILE - 1) / TILE));
+  transpose_kernel<C, TILE><<<grid, TILE * 8, 0, st>>>(static_cast<const C*>(in), static_cast<C*>(out), rows,
+                                                      cols, ld_in, ld_out);
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int xft_version(void) { return 100; }
+
+int64_t xft_max_n(int dtype) { return int64_t(1) << (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128); }
+
+int xft_prepare(int64_t n, int dtype) {
+  if (n < 1) return XFT_EINVALID_SIZE;
+  if (log2_exact(n) < 0 || n > xft_max_n(dtype)) return XFT_ENOTSUP;
+  Tables tb;
+  return get_tables(n, dtype, &tb);
+}
+
+int xft_validate_lct_params(const double* abcd, int64_t count, int64_t stride, int check_unimodular, double tol,
+                            int64_t* bad_row) {
+  const int64_t rows = stride == 0 ? (count > 0 ? 1 : 0) : count;
+  for (int64_t r = 0; r < rows; ++r) {
+    const double* p = abcd + r * stride;
+    if (p[1] == 0.0) {  // xft/lct.py:187-190
+      if (bad_row) *bad_row = r;
+      return XFT_EDEGENERATE;
+    }
+  }
+  if (check_unimodular) {
+    for (int64_t r = 0; r < rows; ++r) {
+      const double* p = abcd + r * stride;
+      const double det = p[0] * p[3] - p[1] * p[2];  // LctParams.det, xft/lct.py:60-64
+      if (!(std::fabs(det - 1.0) <= tol)) {          // xft/lct.py:66-71
+        if (bad_row) *bad_row = r;
+        return XFT_EPARAM;
+      }
+    }
+  }
+  return XFT_OK;
+}
+
+int xft_lct(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd, int64_t abcd_stride,
+            int flags, void* stream) {
+  return run_rows(MODE_LCT, -1, in, out, batch, n, dtype, abcd, abcd_stride, Abcd{0, 0, 0, 0}, flags,
+                  static_cast<cudaStream_t>(stream));
+}
+
+int xft_dft(const void* in, void* out, int64_t batch, int64_t n, int sign, int dtype, void* stream) {
+  if (sign != 1 && sign != -1) return XFT_EPARAM;
+  return run_rows(MODE_DFT, sign, in, out, batch, n, dtype, nullptr, 0, Abcd{0, 0, 0, 0}, 0,
+                  static_cast<cudaStream_t>(stream));
+}
+
+int xft_scaled_fourier(const void* in, void* out, int64_t batch, int64_t n, int dtype, void* stream) {
+  return run_rows(MODE_SCALED, -1, in, out, batch, n, dtype, nullptr, 0, Abcd{0, 0, 0, 0}, 0,
+                  static_cast<cudaStream_t>(stream));
+}
+
+int xft_transpose(const void* in, void* out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out, int dtype,
+                  void* stream) {
+  if (rows < 0 || cols < 0) return XFT_EINVALID_SIZE;
+  if (rows == 0 || cols == 0) return XFT_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  return dtype == XFT_C64 ? launch_transpose<float2>(in, out, rows, cols, ld_in, ld_out, st)
+                          : launch_transpose<double2>(in, out, rows, cols, ld_in, ld_out, st);
+}
+
+int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dtype, const double* abcd_row,
+              const double* abcd_col, void* workspace, void* stream) {
+  if (n_rows < 1 || n_cols < 1) return XFT_EINVALID_SIZE;
+  int rc = xft_validate_lct_params(abcd_row, 1, 0, 1, 1e-10, nullptr);
+  if (!rc) rc = xft_validate_lct_params(abcd_col, 1, 0, 1, 1e-10, nullptr);
+  if (rc) return rc;
+  auto st = static_cast<cudaStream_t>(stream);
+  const Abcd ur{abcd_row[0], abcd_row[1], abcd_row[2], abcd_row[3]};
+  const Abcd uc{abcd_col[0], abcd_col[1], abcd_col[2], abcd_col[3]};
+  // rows -> out ; transpose out -> ws ; rows of ws (= columns) -> out ; transpose out -> ws ; copy-free:
+  // the final transpose writes the caller's buffer.
+  rc = run_rows(MODE_LCT, -1, in, out, n_rows, n_cols, dtype, nullptr, 0, ur, 0, st);
+  if (!rc) rc = xft_transpose(out, workspace, n_rows, n_cols, n_cols, n_rows, dtype, stream);
+  if (!rc) rc = run_rows(MODE_LCT, -1, workspace, out, n_cols, n_rows, dtype, nullptr, 0, uc, 0, st);
+  if (!rc) rc = xft_transpose(out, workspace, n_cols, n_rows, n_rows, n_cols, dtype, stream);
+  if (!rc) {
+    const size_t esz = dtype == XFT_C64 ? 8 : 16;
+    if (cudaMemcpyAsync(out, workspace, esz * n_rows * n_cols, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      rc = XFT_ECUDA;
+  }
+  return rc;
+}
+
+int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+                 int64_t abcd_stride, int flags, int check_unimodular, double tol) {
+  if (n < 1 || batch < 0) return XFT_EINVALID_SIZE;
+  if (dtype != XFT_C64 && dtype != XFT_C128) return XFT_EPARAM;
+  if (log2_exact(n) < 0 || n > xft_max_n(dtype)) return XFT_ENOTSUP;
+  int rc = xft_validate_lct_params(abcd, batch, abcd_stride, check_unimodular, tol, nullptr);
+  if (rc) return rc;
+  if (batch == 0) return XFT_OK;
+  rc = xft_prepare(n, dtype);
+  if (rc) return rc;
+  const size_t esz = dtype == XFT_C64 ? 8 : 16;
+  const size_t row_bytes = esz * (size_t)n;
+  // chunk ~ 16 MiB, at least one row; 3 slots rotate over 3 streams so the
+  // H2D of chunk c+1, the kernel of chunk c and the D2H of chunk c-1 overlap.
+  int64_t chunk = (int64_t)((16u << 20) / row_bytes);
+  if (chunk < 1) chunk = 1;
+  if (chunk > batch) chunk = batch;
+  constexpr int NSLOT = 3;
+  cudaStream_t st[NSLOT] = {};
+  void* dbuf[NSLOT][2] = {};
+  double* dpar[NSLOT] = {};
+  rc = XFT_OK;
+  for (int s = 0; s < NSLOT && !rc; ++s) {
+    if (cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking) != cudaSuccess) rc = XFT_ECUDA;
+    else if (cudaMallocAsync(&dbuf[s][0], row_bytes * chunk, st[s]) != cudaSuccess) rc = XFT_ECUDA;
+    else if (cudaMallocAsync(&dbuf[s][1], row_bytes * chunk, st[s]) != cudaSuccess) rc = XFT_ECUDA;
+    else if (abcd_stride && cudaMallocAsync((void**)&dpar[s], sizeof(double) * abcd_stride * chunk, st[s]) != cudaSuccess)
+      rc = XFT_ECUDA;
+  }
+  const Abcd uni = abcd_stride ? Abcd{0, 0, 0, 0} : Abcd{abcd[0], abcd[1], abcd[2], abcd[3]};
+  for (int64_t r0 = 0, c = 0; r0 < batch && !rc; r0 += chunk, ++c) {
+    const int s = (int)(c % NSLOT);
+    const int64_t rows = (batch - r0 < chunk) ? batch - r0 : chunk;
+    const char* hin = static_cast<const char*>(in) + row_bytes * r0;
+    char* hout = static_cast<char*>(out) + row_bytes * r0;
+    if (cudaMemcpyAsync(dbuf[s][0], hin, row_bytes * rows, cudaMemcpyHostToDevice, st[s]) != cudaSuccess) {
+      rc = XFT_ECUDA;
+      break;
+    }
+    const double* dp = nullptr;
+    if (abcd_stride) {
+      if (cudaMemcpyAsync(dpar[s], abcd + abcd_stride * r0, sizeof(double) * abcd_stride * rows,
+                          cudaMemcpyHostToDevice, st[s]) != cudaSuccess) {
+        rc = XFT_ECUDA;
+        break;
+      }
+      dp = dpar[s];
+    }
+    rc = run_rows(MODE_LCT, -1, dbuf[s][0], dbuf[s][1], rows, n, dtype, dp, abcd_stride, uni, flags, st[s]);
+    if (rc) break;
+    if (cudaMemcpyAsync(hout, dbuf[s][1], row_bytes * rows, cudaMemcpyDeviceToHost, st[s]) != cudaSuccess)
+      rc = XFT_ECUDA;
+  }
+  for (int s = 0; s < NSLOT; ++s) {
+    if (!st[s]) continue;
+    if (dbuf[s][0]) cudaFreeAsync(dbuf[s][0], st[s]);
+    if (dbuf[s][1]) cudaFreeAsync(dbuf[s][1], st[s]);
+    if (dpar[s]) cudaFreeAsync(dpar[s], st[s]);
+    if (cudaStreamSynchronize(st[s]) != cudaSuccess && !rc) rc = XFT_ECUDA;
+    cudaStreamDestroy(st[s]);
+  }
+  return rc;
+}
+
+int64_t xft_mehler_workspace_bytes(int64_t batch, int64_t n) { return 0; }
+
+int xft_validate_mehler_z(const double* z, int64_t count, int64_t stride, int64_t* bad_row) {
+  const int64_t rows = stride == 0 ? (count > 0 ? 1 : 0) : count;
+  for (int64_t r = 0; r < rows; ++r) {
+    const double zr = z[r * stride], zi = z[r * stride + 1];
+    if (std::hypot(zr, zi) > 1.0 + 1e-12) {  // FrftOrder, xft/dense.py:57-58
+      if (bad_row) *bad_row = r;
+      return XFT_EPARAM;
+    }
+    if (std::hypot(zr - 1.0, zi) < 1e-14 || std::hypot(zr + 1.0, zi) < 1e-14) {  // xft/dense.py:129-130
+      if (bad_row) *bad_row = r;
+      return XFT_ESINGULAR;
+    }
+  }
+  return XFT_OK;
+}
+
+int xft_mehler(const void*, void*, int64_t, int64_t, const double*, int64_t, void*, void*) { return XFT_ENOTSUP; }
+
+}  // extern "C"

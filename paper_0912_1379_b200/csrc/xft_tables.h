@@ -1,0 +1,24 @@
+// Immutable per-(device, n, dtype) device tables -- the B200 analogue of an
+// xft DftPlan (xft/fftcore.py:57-105): built once on the host, uploaded once,
+// shared read-only by every launch and every host thread.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace xftb {
+
+struct Tables {
+  const void* tw = nullptr;    // n entries e^{-2 pi i m/n}             (FFT twiddles)
+  const void* ptab = nullptr;  // n entries p_k = e^{i pi ((n-1)k mod 2n)/n}  (xft/kernel.py:51-65)
+  double2 cn{0.0, 0.0};        // C(n)                                    (xft/kernel.py:45-48)
+  double half = 0.0;           // (pi / sqrt(2n)) / 2                     (xft/hermite.py:74-89)
+};
+
+// Returns 0 and fills *out, or an XFT_E* status.  Thread-safe.
+int get_tables(int64_t n, int dtype, Tables* out);
+
+// Host formulas shared with the C-ABI.
+double2 host_kernel_prefactor(int64_t n);
+double host_half_step(int64_t n);
+
+}  // namespace xftb

@@ -1,0 +1,165 @@
+"""Device-level batched operators: torch CUDA tensors in, torch CUDA tensors out.
+
+Each function is a thin shim over one C-ABI entry point (include/xft_b200.h):
+it checks shapes/dtypes, allocates the output, and launches on the current
+torch stream.  torch is only the allocator / stream provider here; all
+arithmetic runs in the hand-written sm_100a kernels of libxft_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidSizeError, ParameterError, ShapeError
+
+UNIMODULAR_TOL = 1e-10
+
+
+def _torch():
+    return _native.require_cuda()
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.complex64:
+        return _native.C64
+    if t.dtype == torch.complex128:
+        return _native.C128
+    raise ParameterError(f"complex64 or complex128 required, got {t.dtype}")
+
+
+def _stream_ptr(device) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _rows_view(values, what="values"):
+    if values.dim() == 1:
+        values = values.unsqueeze(0)
+    if values.dim() != 2:
+        raise ShapeError(f"{what} must be [batch, n], got shape {tuple(values.shape)}")
+    if values.shape[1] < 1:
+        raise InvalidSizeError(f"transform length must be positive, got {values.shape[1]}")
+    if not values.is_cuda:
+        raise ShapeError(f"{what} must be a CUDA tensor")
+    return values.contiguous()
+
+
+def validate_abcd_host(abcd: np.ndarray, check_unimodular=True, tol=UNIMODULAR_TOL) -> None:
+    """Reference-order validation (b == 0 first, then unimodularity) on a host copy."""
+    a = np.ascontiguousarray(abcd, dtype=np.float64)
+    rows = a.reshape(-1, 4)
+    bad = ctypes.c_int64(-1)
+    status = _native.lib().xft_validate_lct_params(
+        a.ctypes.data, rows.shape[0], 4 if rows.shape[0] > 1 or a.ndim == 2 else 0,
+        int(bool(check_unimodular)), float(tol), ctypes.byref(bad))
+    if status:
+        from .errors import raise_for
+        raise_for(status, f"LCT parameters (row {bad.value})")
+
+
+def lct_rows(values, abcd, *, bare_fourier=False, out=None, validate=True,
+             check_unimodular=True, tol=UNIMODULAR_TOL):
+    """Batched fast LCT of the rows of ``values`` ([B, n] complex64/complex128, CUDA).
+
+    ``abcd``: 4 numbers (one quadruple for every row), a [B, 4] array, or a
+    [B, 4] float64 CUDA tensor (per-row parameters, e.g. FrFT angles).
+    Reference semantics: fast_lct (xft/lct.py:168-208) applied to every row.
+    """
+    torch = _torch()
+    v = _rows_view(values)
+    B, n = v.shape
+    if isinstance(abcd, torch.Tensor) and abcd.is_cuda:
+        p_dev = abcd.to(torch.float64).reshape(-1, 4).contiguous()
+        if validate:
+            validate_abcd_host(p_dev.cpu().numpy(), check_unimodular, tol)
+    else:
+        p_host = np.ascontiguousarray(np.asarray(abcd, dtype=np.float64).reshape(-1, 4))
+        if validate:
+            validate_abcd_host(p_host, check_unimodular, tol)
+        p_dev = torch.from_numpy(p_host).to(v.device, non_blocking=False)
+    if p_dev.shape[0] not in (1, B):
+        raise ShapeError(f"abcd has {p_dev.shape[0]} rows for a batch of {B}")
+    stride = 0 if p_dev.shape[0] == 1 else 4
+    if out is None:
+        out = torch.empty_like(v)
+    flags = _native.FLAG_BARE_FOURIER if bare_fourier else 0
+    with torch.cuda.device(v.device):
+        _native.call("xft_lct", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v),
+                     p_dev.data_ptr(), stride, flags, _stream_ptr(v.device))
+    # p_dev may be released now: the caching allocator only reuses its block
+    # in order on this same stream.
+    return out
+
+
+def dft_rows(values, sign: int, *, out=None):
+    """Batched unnormalised DFT (apply_dft, xft/fftcore.py:108-119) of every row."""
+    torch = _torch()
+    if sign not in (1, -1):
+        raise ParameterError(f"direction_sign must be +1 or -1, got {sign!r}")
+    v = _rows_view(values)
+    B, n = v.shape
+    if out is None:
+        out = torch.empty_like(v)
+    with torch.cuda.device(v.device):
+        _native.call("xft_dft", v.data_ptr(), out.data_ptr(), B, n, int(sign), _dtype_code(v),
+                     _stream_ptr(v.device))
+    return out
+
+
+def scaled_fourier_rows(values, *, out=None):
+    """Batched F v = C(n) p DFT(p v) (apply_scaled_fourier, xft/kernel.py:83-95)."""
+    torch = _torch()
+    v = _rows_view(values)
+    B, n = v.shape
+    if out is None:
+        out = torch.empty_like(v)
+    with torch.cuda.device(v.device):
+        _native.call("xft_scaled_fourier", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v),
+                     _stream_ptr(v.device))
+    return out
+
+
+def transpose(values, *, out=None):
+    """out = values.T (tiled device transpose used by the 2-D pass)."""
+    torch = _torch()
+    if values.dim() != 2 or not values.is_cuda:
+        raise ShapeError("transpose needs a 2-D CUDA tensor")
+    v = values.contiguous()
+    r, c = v.shape
+    if out is None:
+        out = torch.empty((c, r), dtype=v.dtype, device=v.device)
+    with torch.cuda.device(v.device):
+        _native.call("xft_transpose", v.data_ptr(), out.data_ptr(), r, c, c, r, _dtype_code(v),
+                     _stream_ptr(v.device))
+    return out
+
+
+def lct_host(values: np.ndarray, abcd, *, bare_fourier=False, out=None,
+             check_unimodular=True, tol=UNIMODULAR_TOL) -> np.ndarray:
+    """End-to-end LCT on HOST arrays through ``xft_lct_host`` (chunked H2D/kernel/D2H pipeline).
+
+    ``values``: [B, n] complex64/complex128 numpy array (pinned memory gives
+    full link bandwidth).  Returns a numpy array of the same dtype.
+    """
+    _torch()
+    v = np.ascontiguousarray(values)
+    if v.ndim == 1:
+        v = v[None, :]
+    if v.dtype == np.complex64:
+        code = _native.C64
+    elif v.dtype == np.complex128:
+        code = _native.C128
+    else:
+        raise ParameterError(f"complex64 or complex128 required, got {v.dtype}")
+    p = np.ascontiguousarray(np.asarray(abcd, dtype=np.float64).reshape(-1, 4))
+    if p.shape[0] not in (1, v.shape[0]):
+        raise ShapeError(f"abcd has {p.shape[0]} rows for a batch of {v.shape[0]}")
+    if out is None:
+        out = np.empty_like(v)
+    flags = _native.FLAG_BARE_FOURIER if bare_fourier else 0
+    _native.call("xft_lct_host", v.ctypes.data, out.ctypes.data, v.shape[0], v.shape[1], code,
+                 p.ctypes.data, 0 if p.shape[0] == 1 else 4, flags, int(bool(check_unimodular)), float(tol))
+    return out

@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path against reference golden vectors and the CPU oracle.
+
+Tolerances (north star, BASELINE.json): per-row relative L2 <= 1e-12 for
+complex128, <= 2e-5 for complex64 (oracle fed the c64 data upcast to c128).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import xft_oracle as O
+from tests.conftest import max_row_rel_l2, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL128 = 1e-12
+TOL64 = 2e-5
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+
+    if not _t.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return _t
+
+
+@pytest.fixture(scope="module")
+def X():
+    import paper_0912_1379_b200 as X
+
+    return X
+
+
+def dev(torch, a, dtype=None):
+    a = np.asarray(a)
+    if dtype is not None:
+        a = a.astype(dtype)
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def lct_gpu(torch, X, abcd, f, dtype=np.complex128, **kw):
+    f = np.atleast_2d(f)
+    return X.ops.lct_rows(dev(torch, f, dtype), abcd, **kw).cpu().numpy()
+
+
+# --------------------------------------------------------------------------
+# golden vectors from the reference
+# --------------------------------------------------------------------------
+LCT_NS = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]
+
+
+@pytest.mark.parametrize("n", LCT_NS)
+def test_lct_golden_c128(torch, X, golden, n):
+    if n > X._native.lib().xft_max_n(1):
+        pytest.skip("c128 row longer than the single-CTA path")
+    f = golden[f"lct_in_n{n}"]
+    P = golden[f"lct_abcd_n{n}"]
+    got = lct_gpu(torch, X, P, np.broadcast_to(f, (P.shape[0], n)))
+    assert max_row_rel_l2(got, golden[f"lct_out_n{n}"]) <= TOL128
+
+
+@pytest.mark.parametrize("n", LCT_NS)
+def test_lct_golden_c64(torch, X, golden, n):
+    f = golden[f"lct_in_n{n}"]
+    P = golden[f"lct_abcd_n{n}"]
+    f64 = np.broadcast_to(f, (P.shape[0], n)).astype(np.complex64)
+    got = lct_gpu(torch, X, P, f64, dtype=np.complex64)
+    _, ref = O.fast_lct_rows(P, f64.astype(np.complex128))
+    assert max_row_rel_l2(got, ref) <= TOL64
+
+
+POW2 = [1, 2, 4, 8, 16, 32, 64, 128, 512, 1024, 2048, 4096, 8192, 16384]
+
+
+@pytest.mark.parametrize("n", POW2)
+def test_dft_golden(torch, X, golden, n):
+    v = golden[f"dft_in_n{n}"]
+    for sign in (1, -1):
+        ref = golden[f"dft_out_n{n}_s{sign}"]
+        if n <= X._native.lib().xft_max_n(1):
+            got = X.ops.dft_rows(dev(torch, v[None]), sign).cpu().numpy()[0]
+            assert rel_l2(got, ref) <= 1e-13, (n, sign)
+        got = X.ops.dft_rows(dev(torch, v[None], np.complex64), sign).cpu().numpy()[0]
+        ref64 = O.dft_rows(v.astype(np.complex64).astype(complex), sign)
+        assert rel_l2(got, ref64) <= 1e-5, (n, sign)
+
+
+def test_dft_known_answers(torch, X):
+    # pkg/tests/test_fftcore.py:45-52
+    for sign in (1, -1):
+        out = X.apply_dft(X.plan_dft(2, sign), [1.0, 1.0])
+        assert np.allclose(out, [2.0, 0.0], atol=1e-15)
+    out = X.apply_dft(X.plan_dft(4, 1), [0, 1, 0, 0])
+    assert np.allclose(out, [1, 1j, -1, -1j], atol=1e-15)
+    assert X.apply_dft(X.plan_dft(1, 1), [3.0 - 1j]).tolist() == [3.0 - 1j]
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 64, 4096])
+def test_scaled_fourier_golden(torch, X, golden, n):
+    got = X.apply_scaled_fourier(golden[f"sf_in_n{n}"])
+    assert rel_l2(got, golden[f"sf_out_n{n}"]) <= TOL128
+
+
+# --------------------------------------------------------------------------
+# BASELINE configs
+# --------------------------------------------------------------------------
+def test_config1(torch, X, golden):
+    got = lct_gpu(torch, X, golden["cfg1_abcd"], golden["cfg1_in"])[0]
+    assert rel_l2(got, golden["cfg1_out"]) <= TOL128
+    assert rel_l2(got, golden["cfg1_dense_out"]) <= TOL128
+
+
+def test_config2_rows_golden(torch, X, golden):
+    got = lct_gpu(torch, X, golden["cfg2_abcd"], golden["cfg2_in"])
+    assert max_row_rel_l2(got, golden["cfg2_out"]) <= TOL128
+    got = lct_gpu(torch, X, golden["cfg2_abcd"], golden["cfg2_in"], dtype=np.complex64)
+    assert max_row_rel_l2(got, golden["cfg2_out_c64in"]) <= TOL64
+
+
+def test_config4_rows_golden(torch, X, golden):
+    got = lct_gpu(torch, X, (0.0, 1.0, -1.0, 0.0), golden["cfg4_in"], dtype=np.complex64)
+    assert max_row_rel_l2(got, golden["cfg4_out"]) <= TOL64
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.complex64, TOL64), (np.complex128, TOL128)])
+def test_config2_full_batch(torch, X, dtype, tol):
+    """Full 4096 x 4096 batch: oracle on sampled rows (incl. the extreme-phase rows) + norm identity on all rows."""
+    from paper_0912_1379_b200 import workloads
+
+    c2 = workloads.config2(dtype=dtype)
+    got_t = X.ops.lct_rows(dev(torch, c2.values), c2.abcd)
+    alpha = c2.extra["alpha"]
+    rows = sorted(set([0, 1, 2, 4095, int(np.argmin(alpha)), int(np.argmax(alpha)),
+                       int(np.argmin(np.abs(alpha - math.pi / 2)))] + list(range(100, 4096, 397))))
+    got = got_t[rows].cpu().numpy()
+    _, ref = O.fast_lct_rows(c2.abcd[rows], c2.values[rows].astype(np.complex128))
+    assert max_row_rel_l2(got, ref) <= tol
+    # ||G||^2 = pi/(4|b|) ||f||^2 on every row
+    f = dev(torch, c2.values).to(torch.complex128)
+    lhs = (got_t.to(torch.complex128).abs() ** 2).sum(dim=1).cpu().numpy()
+    rhs = (math.pi / (4 * np.abs(c2.abcd[:, 1]))) * (f.abs() ** 2).sum(dim=1).cpu().numpy()
+    assert np.max(np.abs(lhs / rhs - 1)) <= (1e-12 if dtype == np.complex128 else 1e-4)
+
+
+def test_config4_full_batch_and_quadrature(torch, X):
+    from paper_0912_1379_b200 import workloads
+
+    c4 = workloads.config4()
+    got_t = X.ops.lct_rows(dev(torch, c4.values), c4.abcd)
+    rows = [0, 1, 777, 65535]
+    got = got_t[rows].cpu().numpy()
+    _, ref = O.fast_lct_rows(c4.abcd, c4.values[rows].astype(np.complex128))
+    assert max_row_rel_l2(got, ref) <= TOL64
+    # the continuous transform of the Hermite-Gaussian mixture (quadrature error report)
+    cf = workloads.config4_closed_form(c4.extra["coeffs"][rows])
+    lo, hi = 1024 // 10, 9 * 1024 // 10
+    assert np.max(np.abs(got[:, lo:hi] - cf[:, lo:hi])) <= 1e-4 * np.max(np.abs(cf))
+
+
+# --------------------------------------------------------------------------
+# reference API behaviour (pkg/tests/test_lct.py, test_fftcore.py analogues)
+# --------------------------------------------------------------------------
+def test_fourier_and_frft_golden(torch, X, golden):
+    for n in (8, 96, 256):
+        g = X.Signal(X.asymptotic_zeros(n), golden[f"fourier_in_n{n}"]) if n != 96 else None
+        if g is None:
+            continue  # n = 96 is not a power of two (chirp-z route, see test_bluestein)
+        assert rel_l2(X.xft_fourier(g).values, golden[f"fourier_out_n{n}"]) <= TOL128
+        for t, ref in zip((0.3, math.pi / 2, -0.7, 3.0), golden[f"frft_out_n{n}"]):
+            assert rel_l2(X.fast_frft(t, g).values, ref) <= TOL128
+
+
+def test_quarter_turn_bitwise_equals_fourier(torch, X):
+    rng = np.random.default_rng(31)
+    g = X.Signal(X.asymptotic_zeros(64), rng.normal(size=64) + 1j * rng.normal(size=64))
+    a = X.fast_frft(math.pi / 2, g)
+    b = X.fast_lct(X.LctParams.fourier(), g)
+    assert np.array_equal(a.values, b.values)
+
+
+def test_zero_in_zero_out(torch, X):
+    for n in (16, 1024):
+        g = X.Signal(X.asymptotic_zeros(n), np.zeros(n, dtype=complex))
+        assert np.all(X.fast_lct(X.LctParams(1.0, 2.0, 0.5, 2.0), g).values == 0)
+        assert np.all(X.xft_fourier(g).values == 0)
+
+
+def test_deterministic_and_input_untouched(torch, X):
+    rng = np.random.default_rng(4)
+    v = dev(torch, rng.normal(size=(64, 4096)) + 1j * rng.normal(size=(64, 4096)), np.complex64)
+    keep = v.clone()
+    P = np.array([X.LctParams.frft(0.1 + 0.01 * i).as_tuple() for i in range(64)])
+    a = X.ops.lct_rows(v, P)
+    b = X.ops.lct_rows(v, P)
+    assert torch.equal(a, b)
+    assert torch.equal(v, keep)
+
+
+def test_output_nodes_and_validation_order(torch, X):
+    g = X.Signal(X.asymptotic_zeros(4), np.ones(4, dtype=complex))
+    with pytest.raises(X.DegenerateParameterError):
+        X.fast_lct(X.LctParams(1.0, 0.0, 0.0, 1.0), g)
+    with pytest.raises(X.ParameterError):
+        X.fast_lct(X.LctParams(1.0, 1.0, 1.0, 1.0), g)
+    X.fast_lct(X.LctParams(1.0, 1.0, 1.0, 1.0), g, check_unimodular=False)
+    nodes = np.linspace(-1, 1, 8)
+    bad = X.HermiteGrid(n=8, nodes=nodes, spacing=nodes[1] - nodes[0])
+    with pytest.raises(X.GridMismatchError):
+        X.fast_lct(X.LctParams.fourier(), X.Signal(bad, np.ones(8, dtype=complex)))
+    with pytest.raises(X.ShapeError):
+        X.fast_lct(X.LctParams.fourier(), X.Signal(X.asymptotic_zeros(8), np.ones(8)),
+                   plan=X.plan_dft(16, -1))
+    with pytest.raises(X.DegenerateParameterError):
+        X.fast_frft(0.0, g)
+    rng = np.random.default_rng(0)
+    sig = X.Signal(X.asymptotic_zeros(32), rng.normal(size=32) + 0j)
+    p = X.LctParams(1.0, -2.5, (0.6 - 1) / -2.5, 0.6)
+    res = X.fast_lct(p, sig)
+    assert np.max(np.abs(res.output_nodes - (4 * p.b / np.pi) * sig.grid.nodes)) <= 1e-13
+
+
+def test_batch_param_errors(torch, X):
+    v = dev(torch, np.ones((3, 8)), np.complex128)
+    P = np.array([X.LctParams.frft(0.3).as_tuple(), (1.0, 0.0, 0.0, 1.0), (1.0, 1.0, 1.0, 1.0)])
+    with pytest.raises(X.DegenerateParameterError):   # b == 0 checked before unimodularity
+        X.ops.lct_rows(v, P)
+    P[1] = X.LctParams.frft(0.2).as_tuple()
+    with pytest.raises(X.ParameterError):
+        X.ops.lct_rows(v, P)
+
+
+def test_host_end_to_end_matches_device(torch, X):
+    from paper_0912_1379_b200 import workloads
+
+    c2 = workloads.config2(rows=512, n=4096, dtype=np.complex64, row_limit=None)
+    host_in = torch.from_numpy(c2.values).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    X.ops.lct_host(host_in.numpy(), c2.abcd, out=host_out.numpy())
+    ref = X.ops.lct_rows(dev(torch, c2.values), c2.abcd).cpu()
+    assert torch.equal(host_out, ref)
+    with pytest.raises(X.DegenerateParameterError):
+        X.ops.lct_host(c2.values[:2], (1.0, 0.0, 0.0, 1.0))
+
+
+def test_empty_batch(torch, X):
+    v = torch.empty((0, 64), dtype=torch.complex128, device="cuda")
+    assert X.ops.lct_rows(v, (0.0, 1.0, -1.0, 0.0)).shape == (0, 64)
+
+
+def test_lct2d_golden(torch, X, golden):
+    from paper_0912_1379_b200 import lct2d
+
+    f = dev(torch, golden["lct2d_in"])
+    got = lct2d.lct2d(f, (1.0, 0.25, 0.0, 1.0), (1.0, 0.25, 0.0, 1.0)).cpu().numpy()
+    assert rel_l2(got, golden["lct2d_out"]) <= TOL128
