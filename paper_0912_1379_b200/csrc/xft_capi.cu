@@ -6,7 +6,7 @@
 #include <utility>
 
 #include "../../include/xft_b200.h"
-#include "xft_rows.cuh"
+#include "xft_pipe.cuh"
 #include "xft_tables.h"
 
 using namespace xftb;
@@ -15,13 +15,6 @@ namespace {
 
 constexpr int MAXLOG_C64 = 14;   // 16384 x 8 B = 128 KiB per row in shared memory
 constexpr int MAXLOG_C128 = 13;  //  8192 x 16 B = 128 KiB
-
-template <class C, int L>
-constexpr int pick_e() {
-  if (L == 0) return 1;
-  if (sizeof(C) == 8) return L >= 4 ? 16 : (1 << L);        // c64: radix-16 passes
-  return L >= 13 ? 16 : (L >= 3 ? 8 : (1 << L));           // c128: radix-8 (16 at 8192)
-}
 
 struct LaunchArgs {
   const void* in;
@@ -37,19 +30,69 @@ struct LaunchArgs {
 
 using LaunchFn = int (*)(const LaunchArgs&);
 
+// single-pass sizes (n <= radix): one register DFT per thread, no exchange
 template <class C, int L, int MODE, int SIGN>
-int launch_rows(const LaunchArgs& a) {
-  using Cfg = RowCfg<C, L, pick_e<C, L>(), MODE, SIGN>;
+int launch_small(const LaunchArgs& a) {
+  using Cfg = RowCfg<C, L, (1 << L), MODE, SIGN>;
   auto kern = xft_rows_kernel<Cfg>;
-  if (Cfg::SMEM > 48 * 1024) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
-      return XFT_ECUDA;
-  }
   const long long grid = (a.batch + Cfg::ROWS - 1) / Cfg::ROWS;
-  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
+  kern<<<(unsigned)grid, Cfg::THREADS, 0, a.st>>>(
       static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
       static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.cn, a.tb.half, a.flags);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+template <class C, int L>
+struct PipeShape {
+  static constexpr int E = pipe_radix(sizeof(C) == 8 ? XFT_C64 : XFT_C128, L);
+  static constexpr int TR = (1 << L) / E;
+  static constexpr int TARGET = sizeof(C) == 8 ? 256 : 512;  // threads per CTA
+  static constexpr int ROWS = TR >= TARGET ? 1 : TARGET / TR;
+  static constexpr size_t TILE_BYTES = size_t(ROWS) * (size_t(1) << L) * sizeof(C);
+  static constexpr size_t STATIC = 2 * ROWS * (sizeof(C) == 8 ? sizeof(Coef64) : sizeof(Coef128)) + 256;
+  static constexpr size_t BUDGET = 200 * 1024 - STATIC - (sizeof(C) == 16 ? 4096 : 0);
+  static constexpr int STAGES = BUDGET / TILE_BYTES >= 3 ? 3 : (BUDGET / TILE_BYTES >= 2 ? 2 : 1);
+};
+
+template <class C, int L, int MODE, int SIGN>
+int launch_pipe(const LaunchArgs& a) {
+  using SH = PipeShape<C, L>;
+  using Cfg = PipeCfg<C, L, SH::E, MODE, SIGN, SH::ROWS, SH::STAGES>;
+  auto kern = xft_pipe_kernel<Cfg>;
+  static int occ_cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
+    return XFT_ECUDA;
+  int& occ = occ_cache[dev & 63];
+  if (occ == 0) {
+    int o = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::THREADS, Cfg::SMEM) != cudaSuccess)
+      return XFT_ECUDA;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return XFT_ECUDA;
+    occ = (o < 1 ? 1 : o) * sms;
+  }
+  const long long tiles = (a.batch + Cfg::ROWS - 1) / Cfg::ROWS;
+  const long long grid = tiles < occ ? tiles : occ;
+  RowConst kc;
+  kc.half = a.tb.half;
+  kc.cnabs = M_PI / std::sqrt(2.0 * double(1 << L));
+  kc.cnred = (long long)(((__int128)((1 << L) - 1) * ((1 << L) - 1)) % (4 * (__int128)(1 << L)));
+  kc.log2n = L;
+  kc.flags = a.flags;
+  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
+      static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
+      static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), static_cast<const double2*>(a.tb.gtab),
+      a.tb.cn, kc);
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+template <class C, int L, int MODE, int SIGN>
+int launch_rows(const LaunchArgs& a) {
+  if constexpr ((1 << L) <= pipe_radix(sizeof(C) == 8 ? XFT_C64 : XFT_C128, L))
+    return launch_small<C, L, MODE, SIGN>(a);
+  else
+    return launch_pipe<C, L, MODE, SIGN>(a);
 }
 
 template <class C, int MODE, int SIGN, int... Ls>

@@ -29,15 +29,38 @@ struct Entry {
 };
 
 std::mutex g_mu;
+std::map<int, void*> g_gtab;
 std::map<std::tuple<int, int64_t, int>, Entry> g_tables;
 
+const long double PI_L = 3.141592653589793238462643383279502884L;
+
+// Pass-major twiddles: for pass p >= 1 (NS = R0 E^(p-1)), entry (t-1)*NS + k
+// holds e^{-2 pi i t k / (NS E)}; layout identical to PipeCfg::twoff.
 template <class T2, class R>
-void fill(std::vector<T2>& tw, std::vector<T2>& pt, int64_t n) {
-  const long double PI_L = 3.141592653589793238462643383279502884L;
+void fill_twiddles(std::vector<T2>& tw, int64_t n, int E) {
+  int l = 0, le = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  while ((1 << le) < E) ++le;
+  tw.clear();
+  if (n <= E) return;  // single-pass sizes use no table
+  const int npass = (l + le - 1) / le;
+  const int64_t r0 = int64_t(1) << (l - (npass - 1) * le);
+  int64_t ns = r0;
+  for (int p = 1; p < npass; ++p, ns *= E) {
+    for (int t = 1; t < E; ++t)
+      for (int64_t k = 0; k < ns; ++k) {
+        const long double th = 2.0L * PI_L * (long double)(t * k) / (long double)(ns * E);
+        T2 w;
+        w.x = (R)cosl(th);
+        w.y = (R)(-sinl(th));
+        tw.push_back(w);
+      }
+  }
+}
+
+template <class T2, class R>
+void fill(std::vector<T2>& pt, int64_t n) {
   for (int64_t m = 0; m < n; ++m) {
-    const long double th = 2.0L * PI_L * (long double)m / (long double)n;
-    tw[m].x = (R)cosl(th);
-    tw[m].y = (R)(-sinl(th));
     // p_k = exp(+i pi ((n-1)k mod 2n) / n)   (xft/kernel.py:51-65)
     const int64_t red = (int64_t)(((__int128)(n - 1) * m) % (2 * (__int128)n));
     const long double ph = PI_L * (long double)red / (long double)n;
@@ -58,25 +81,45 @@ int get_tables(int64_t n, int dtype, Tables* out) {
   auto it = g_tables.find(key);
   if (it == g_tables.end()) {
     Entry e;
-    const size_t esz = dtype == XFT_C64 ? sizeof(float2) : sizeof(double2);
-    const size_t bytes = esz * (size_t)n;
-    if (cudaMalloc(&e.tw, bytes) != cudaSuccess) return XFT_ECUDA;
-    if (cudaMalloc(&e.ptab, bytes) != cudaSuccess) return XFT_ECUDA;
-    cudaError_t r1, r2;
+    int l = 0;
+    while ((int64_t(1) << l) < n) ++l;
+    const int E = pipe_radix(dtype, l);
+    cudaError_t r1 = cudaSuccess, r2 = cudaSuccess;
+    auto upload = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+      if (bytes == 0) bytes = 16;  // keep a valid pointer for empty tables
+      cudaError_t r = cudaMalloc(dst, bytes);
+      if (r != cudaSuccess) return r;
+      return src ? cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
     if (dtype == XFT_C64) {
-      std::vector<float2> tw(n), pt(n);
-      fill<float2, float>(tw, pt, n);
-      r1 = cudaMemcpy(e.tw, tw.data(), bytes, cudaMemcpyHostToDevice);
-      r2 = cudaMemcpy(e.ptab, pt.data(), bytes, cudaMemcpyHostToDevice);
+      std::vector<float2> tw, pt(n);
+      fill_twiddles<float2, float>(tw, n, E);
+      fill<float2, float>(pt, n);
+      r1 = upload(&e.tw, tw.empty() ? nullptr : tw.data(), tw.size() * sizeof(float2));
+      r2 = upload(&e.ptab, pt.data(), pt.size() * sizeof(float2));
     } else {
-      std::vector<double2> tw(n), pt(n);
-      fill<double2, double>(tw, pt, n);
-      r1 = cudaMemcpy(e.tw, tw.data(), bytes, cudaMemcpyHostToDevice);
-      r2 = cudaMemcpy(e.ptab, pt.data(), bytes, cudaMemcpyHostToDevice);
+      std::vector<double2> tw, pt(n);
+      fill_twiddles<double2, double>(tw, n, E);
+      fill<double2, double>(pt, n);
+      r1 = upload(&e.tw, tw.empty() ? nullptr : tw.data(), tw.size() * sizeof(double2));
+      r2 = upload(&e.ptab, pt.data(), pt.size() * sizeof(double2));
     }
     if (r1 != cudaSuccess || r2 != cudaSuccess) return XFT_ECUDA;
     it = g_tables.emplace(key, e).first;
   }
+  auto gt = g_gtab.find(dev);
+  if (gt == g_gtab.end()) {
+    std::vector<double2> g(256);
+    for (int m = 0; m < 256; ++m) {
+      const long double th = 2.0L * PI_L * (long double)m / 256.0L;
+      g[m] = make_double2((double)cosl(th), (double)sinl(th));
+    }
+    void* d = nullptr;
+    if (cudaMalloc(&d, 256 * sizeof(double2)) != cudaSuccess) return XFT_ECUDA;
+    if (cudaMemcpy(d, g.data(), 256 * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess) return XFT_ECUDA;
+    gt = g_gtab.emplace(dev, d).first;
+  }
+  out->gtab = gt->second;
   out->tw = it->second.tw;
   out->ptab = it->second.ptab;
   return XFT_OK;

@@ -7,9 +7,14 @@
 
 namespace xftb {
 
+// Radix (elements per thread) of the pipelined kernel for (dtype, log2 n);
+// shared by the host table builder and the kernel instantiation.
+constexpr int pipe_radix(int dtype, int l) { return dtype == 0 ? 16 : (l >= 13 ? 16 : 8); }
+
 struct Tables {
-  const void* tw = nullptr;    // n entries e^{-2 pi i m/n}             (FFT twiddles)
+  const void* tw = nullptr;    // pass-major twiddles of the pipelined kernel (see xft_pipe.cuh)
   const void* ptab = nullptr;  // n entries p_k = e^{i pi ((n-1)k mod 2n)/n}  (xft/kernel.py:51-65)
+  const void* gtab = nullptr;  // 256 entries e^{2 pi i m/256} (c128 chirp table)
   double2 cn{0.0, 0.0};        // C(n)                                    (xft/kernel.py:45-48)
   double half = 0.0;           // (pi / sqrt(2n)) / 2                     (xft/hermite.py:74-89)
 };
