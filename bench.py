@@ -234,51 +234,56 @@ def run_ours(args, rank, world, local_rank):
             vin = torch.from_numpy(v).to(dev)
             s.append((tag, vin, torch.empty_like(vin), torch.from_numpy(np.ascontiguousarray(p)).to(dev)))
         sets.append(s)
-    stream = torch.cuda.current_stream(dev)
-
-    def step(i, evs=None):
-        for k, (tag, vin, vout, p) in enumerate(sets[i % nsets]):
-            if evs is not None:
-                evs[k][0].record(stream)
-            ops.lct_rows(vin, p, out=vout, validate=False)
-            if evs is not None:
-                evs[k][1].record(stream)
+    stream = torch.cuda.Stream(dev)
 
     # validate once (reference order) outside the timed region
     for _, v, p in work:
         ops.validate_abcd_host(p)
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
+
+    # The step is captured once per buffer set as a CUDA graph (per-row
+    # coefficient kernel + transform kernel per dtype), so the timed loop is
+    # free of Python launch overhead: it replays graphs on one stream.
+    def capture(items):
+        with torch.cuda.stream(stream):  # warm (tables, attributes, allocator pools)
+            for tag, vin, vout, p in items:
+                ops.lct_rows(vin, p, out=vout, validate=False)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for tag, vin, vout, p in items:
+                ops.lct_rows(vin, p, out=vout, validate=False)
+        return g
+
+    step_graphs = [capture(sets[i]) for i in range(nsets)]
+    kern_graphs = [[capture([sets[i][k]]) for i in range(nsets)] for k in range(len(work))]
+    launches_per_step = 2 * len(work)  # coefficient kernel + transform kernel per dtype
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
-    # per-kernel timing pass (events around every launch)
-    kev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-            for _ in work] for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        step(i, kev[i])
-    torch.cuda.synchronize()
-    kern_ms = [sum(kev[i][k][0].elapsed_time(kev[i][k][1]) for i in range(args.steps)) / args.steps
-               for k in range(len(work))]
+    def timed(graphs, n):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(n):
+            graphs[i % nsets].replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return e0.elapsed_time(e1)
 
-    # main timed region: K steps bracketed by barrier + synchronize
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        barrier()
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step_graphs[i % nsets].replay()
         torch.cuda.synchronize()
-        t0.record(stream)
-        for i in range(args.steps):
-            step(i)
-        t1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-    total_ms = t0.elapsed_time(t1)
+        # per-kernel averages (same replay scheme, one dtype at a time)
+        kern_ms = [timed(kern_graphs[k], args.steps) / args.steps for k in range(len(work))]
+        # main timed region: K steps bracketed by barrier + synchronize
+        with ClockSampler(local_rank) as clk:
+            total_ms = timed(step_graphs, args.steps)
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -323,7 +328,7 @@ def run_ours(args, rank, world, local_rank):
                     "traffic": traffic.get(f"{args.config}_{tag}")}
     dom = max(per, key=lambda t: per[t]["kernel_ms"])
     roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
-            "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"xft_rows_kernel {dom}",
+            "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"xft_pipe_kernel {dom}",
             "peak_source": peak_kind,
             "step_achieved": bytes_of(work) / (ms_per_step * 1e-3) / 1e9}
 
@@ -343,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof, "per_dtype": per, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "Msamples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "api": "paper_0912_1379_b200.ops.lct_host -> xft_lct_host"},
-        "gpu_launches": len(work) * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

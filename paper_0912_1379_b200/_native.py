@@ -14,7 +14,7 @@ import threading
 from .errors import XftError, raise_for
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libxft_b200.so")
+LIB_PATH = os.environ.get("XFT_LIB") or os.path.join(_HERE, "libxft_b200.so")  # XFT_LIB: tuning builds only
 
 C64 = 0
 C128 = 1

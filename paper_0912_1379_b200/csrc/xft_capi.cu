@@ -42,22 +42,51 @@ int launch_small(const LaunchArgs& a) {
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
 }
 
+// Shape of the pipelined kernel per (dtype, n): threads per CTA, resident CTAs
+// per SM (register budget), ring depth.  Overridable at build time for tuning.
+#ifndef XFT_C64_TARGET
+#define XFT_C64_TARGET 256
+#endif
+#ifndef XFT_C64_MINB
+#define XFT_C64_MINB 4
+#endif
+#ifndef XFT_C64_MAXST
+#define XFT_C64_MAXST 1
+#endif
+#ifndef XFT_C128_TARGET
+#define XFT_C128_TARGET 256
+#endif
+#ifndef XFT_C128_MINB
+#define XFT_C128_MINB 2
+#endif
+#ifndef XFT_C128_MAXST
+#define XFT_C128_MAXST 1
+#endif
 template <class C, int L>
 struct PipeShape {
-  static constexpr int E = pipe_radix(sizeof(C) == 8 ? XFT_C64 : XFT_C128, L);
+  static constexpr bool C64 = sizeof(C) == 8;
+  static constexpr int E = pipe_radix(C64 ? XFT_C64 : XFT_C128, L);
   static constexpr int TR = (1 << L) / E;
-  static constexpr int TARGET = sizeof(C) == 8 ? 256 : 512;  // threads per CTA
-  static constexpr int ROWS = TR >= TARGET ? 1 : TARGET / TR;
+  static constexpr int TARGET = C64 ? XFT_C64_TARGET : XFT_C128_TARGET;  // threads per CTA
+  static constexpr int ROWS = TR >= TARGET ? 1 : (TARGET / TR > 64 ? 64 : TARGET / TR);
+  static constexpr int MINB0 = C64 ? XFT_C64_MINB : XFT_C128_MINB;
   static constexpr size_t TILE_BYTES = size_t(ROWS) * (size_t(1) << L) * sizeof(C);
-  static constexpr size_t STATIC = 2 * ROWS * (sizeof(C) == 8 ? sizeof(Coef64) : sizeof(Coef128)) + 256;
-  static constexpr size_t BUDGET = 200 * 1024 - STATIC - (sizeof(C) == 16 ? 4096 : 0);
-  static constexpr int STAGES = BUDGET / TILE_BYTES >= 3 ? 3 : (BUDGET / TILE_BYTES >= 2 ? 2 : 1);
+  static constexpr size_t STATIC = 2 * ROWS * (C64 ? sizeof(Coef64) : sizeof(Coef128)) + 256;
+  static constexpr size_t TAB = C64 ? 0 : XFT_C128_TABCOPIES * 256 * 16;
+  // resident CTAs per SM: requested, capped by threads (2048/SM) and by one stage of smem
+  static constexpr int MINB_T = 65536 / (TR * ROWS * 64);  // keep >= 64 registers per thread
+  static constexpr int MINB_S = int((226 * 1024) / (TILE_BYTES + TAB + STATIC + 1024));
+  static constexpr int MINB1 = MINB0 < MINB_T ? MINB0 : MINB_T;
+  static constexpr int MINB = (MINB1 < MINB_S ? MINB1 : MINB_S) < 1 ? 1 : (MINB1 < MINB_S ? MINB1 : MINB_S);
+  static constexpr size_t BUDGET = (226 * 1024) / MINB - 1024 - STATIC - TAB;
+  static constexpr int MAXST = C64 ? XFT_C64_MAXST : XFT_C128_MAXST;
+  static constexpr int STAGES = BUDGET / TILE_BYTES >= MAXST ? MAXST : (BUDGET / TILE_BYTES >= 2 ? 2 : 1);
 };
 
 template <class C, int L, int MODE, int SIGN>
 int launch_pipe(const LaunchArgs& a) {
   using SH = PipeShape<C, L>;
-  using Cfg = PipeCfg<C, L, SH::E, MODE, SIGN, SH::ROWS, SH::STAGES>;
+  using Cfg = PipeCfg<C, L, SH::E, MODE, SIGN, SH::ROWS, SH::STAGES, SH::MINB>;
   auto kern = xft_pipe_kernel<Cfg>;
   static int occ_cache[64] = {0};
   int dev = 0;
@@ -80,10 +109,21 @@ int launch_pipe(const LaunchArgs& a) {
   kc.cnred = (long long)(((__int128)((1 << L) - 1) * ((1 << L) - 1)) % (4 * (__int128)(1 << L)));
   kc.log2n = L;
   kc.flags = a.flags;
+  using Coef = typename Cfg::Coef;
+  Coef* coefs = nullptr;
+  int per_row = 0;
+  if constexpr (MODE == MODE_LCT) {
+    // per-row coefficients (divisions, branch cuts, phase offsets) once per row,
+    // streamed into shared memory by the same TMA as the rows
+    per_row = (a.abcd != nullptr && a.stride != 0) ? 1 : 0;
+    const long long nco = per_row ? a.batch : 1;
+    if (cudaMallocAsync((void**)&coefs, sizeof(Coef) * nco, a.st) != cudaSuccess) return XFT_ECUDA;
+    xft_coef_kernel<Coef><<<(unsigned)((nco + 127) / 128), 128, 0, a.st>>>(coefs, nco, a.abcd, a.stride, a.uni, kc);
+  }
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
-      static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
-      static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), static_cast<const double2*>(a.tb.gtab),
-      a.tb.cn, kc);
+      static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, coefs, per_row,
+      static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc);
+  if (coefs) cudaFreeAsync(coefs, a.st);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
 }
 

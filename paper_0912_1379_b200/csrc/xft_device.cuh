@@ -37,6 +37,46 @@ template <int SIGN, class C> __device__ __forceinline__ C rot(C a) {
 }
 template <class C, class S> __device__ __forceinline__ C cscale(C a, S s) { return mk(a.x * s, a.y * s); }
 
+// ---- packed fp32x2 (sm_100 FADD2/FMUL2/FFMA2): one instruction per complex add ----
+// The operand swaps/broadcasts/single-lane negations below are folded by ptxas
+// into the .F32x2.LO_HI / .F32 / .NP operand modifiers of the packed ops.
+__device__ __forceinline__ unsigned long long pk2(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ float2 p_add(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 p_sub(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 p_mul(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 p_fma(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return p_add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return p_sub(a, b); }
+// (a.x + i a.y)(b.x + i b.y) = b.x (a.x, a.y) + b.y (-a.y, a.x): FMUL2 + FFMA2
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return p_fma(make_float2(-a.y, a.x), make_float2(b.y, b.y), p_mul(a, make_float2(b.x, b.x)));
+}
+
 // ---------------------------------------------------------------------------
 // e^{i phi}
 // ---------------------------------------------------------------------------
@@ -172,6 +212,20 @@ template <int SIGN, int K, class C> __device__ __forceinline__ C w8(C a) {
   return mk((cs * a.x - sn * a.y) * h, (cs * a.y + sn * a.x) * h);
 }
 
+template <int SIGN, int K> __device__ __forceinline__ float2 w8(float2 a) {
+  constexpr int k = K & 7;
+  if constexpr (k == 0) return a;
+  else if constexpr (k == 2) return rot<SIGN>(a);
+  else if constexpr (k == 4) return make_float2(-a.x, -a.y);
+  else if constexpr (k == 6) return rot<-SIGN>(a);
+  else {
+    const float h = 0.70710678118654752440f;
+    const float cs = (k == 1 || k == 7) ? h : -h;
+    const float sn = ((k == 1 || k == 3) ? h : -h) * SIGN;
+    return p_fma(make_float2(-a.y, a.x), make_float2(sn, sn), p_mul(a, make_float2(cs, cs)));
+  }
+}
+
 template <int SIGN, class C> __device__ __forceinline__ void dft8(C* v) {
   // radix-2 split: even / odd halves then combine with w8^k
   C e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
@@ -198,6 +252,16 @@ template <int SIGN, int K, class C> __device__ __forceinline__ C w16odd(C a) {
   return mk(a.x * c - a.y * s, a.x * s + a.y * c);
 }
 
+template <int SIGN, int K> __device__ __forceinline__ float2 w16odd(float2 a) {
+  constexpr int k = K;
+  const float c = (k == 1) ? 0.92387953251128675613f : (k == 3) ? 0.38268343236508977173f
+                : (k == 5) ? -0.38268343236508977173f : -0.92387953251128675613f;
+  const float s0 = (k == 1) ? 0.38268343236508977173f : (k == 3) ? 0.92387953251128675613f
+                 : (k == 5) ? 0.92387953251128675613f : 0.38268343236508977173f;
+  const float s = SIGN * s0;
+  return p_fma(make_float2(-a.y, a.x), make_float2(s, s), p_mul(a, make_float2(c, c)));
+}
+
 template <int SIGN, class C> __device__ __forceinline__ void dft16(C* v) {
   C e[8], o[8];
 #pragma unroll
@@ -218,11 +282,50 @@ template <int SIGN, class C> __device__ __forceinline__ void dft16(C* v) {
   }
 }
 
+// w32^k (k = 1..15), cos and sin of 2 pi k / 32
+__constant__ const double kW32c[16] = {1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452,
+                                       0.7071067811865476, 0.5555702330196023, 0.38268343236508984,
+                                       0.19509032201612833, 0.0, -0.19509032201612833, -0.38268343236508984,
+                                       -0.5555702330196023, -0.7071067811865476, -0.8314696123025452,
+                                       -0.9238795325112867, -0.9807852804032304};
+__constant__ const double kW32s[16] = {0.0, 0.19509032201612825, 0.3826834323650898, 0.5555702330196022,
+                                       0.7071067811865475, 0.8314696123025452, 0.9238795325112867,
+                                       0.9807852804032304, 1.0, 0.9807852804032304, 0.9238795325112867,
+                                       0.8314696123025452, 0.7071067811865475, 0.5555702330196022,
+                                       0.3826834323650898, 0.19509032201612825};
+template <int SIGN, int K> __device__ __forceinline__ double2 w32(double2 a) {
+  const double c = kW32c[K], s = SIGN * kW32s[K];
+  return make_double2(a.x * c - a.y * s, a.x * s + a.y * c);
+}
+template <int SIGN, int K> __device__ __forceinline__ float2 w32(float2 a) {
+  const float c = (float)kW32c[K], s = (float)(SIGN * kW32s[K]);
+  return p_fma(make_float2(-a.y, a.x), make_float2(s, s), p_mul(a, make_float2(c, c)));
+}
+
+template <int SIGN, class C> __device__ __forceinline__ void dft32(C* v) {
+  C e[16], o[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
+  dft16<SIGN>(e);
+  dft16<SIGN>(o);
+  o[1] = w32<SIGN, 1>(o[1]);   o[2] = w32<SIGN, 2>(o[2]);   o[3] = w32<SIGN, 3>(o[3]);
+  o[4] = w32<SIGN, 4>(o[4]);   o[5] = w32<SIGN, 5>(o[5]);   o[6] = w32<SIGN, 6>(o[6]);
+  o[7] = w32<SIGN, 7>(o[7]);   o[8] = rot<SIGN>(o[8]);      o[9] = w32<SIGN, 9>(o[9]);
+  o[10] = w32<SIGN, 10>(o[10]); o[11] = w32<SIGN, 11>(o[11]); o[12] = w32<SIGN, 12>(o[12]);
+  o[13] = w32<SIGN, 13>(o[13]); o[14] = w32<SIGN, 14>(o[14]); o[15] = w32<SIGN, 15>(o[15]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[i] = cadd(e[i], o[i]);
+    v[i + 16] = csub(e[i], o[i]);
+  }
+}
+
 template <int R, int SIGN, class C> __device__ __forceinline__ void dft_r(C* v) {
   if constexpr (R == 2) dft2<SIGN>(v[0], v[1]);
   else if constexpr (R == 4) dft4<SIGN>(v[0], v[1], v[2], v[3]);
   else if constexpr (R == 8) dft8<SIGN>(v);
   else if constexpr (R == 16) dft16<SIGN>(v);
+  else if constexpr (R == 32) dft32<SIGN>(v);
 }
 
 }  // namespace xftb

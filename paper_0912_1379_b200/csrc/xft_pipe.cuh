@@ -1,6 +1,6 @@
 // K1 (production path): persistent, TMA-pipelined batched chirp-DFT-chirp.
 //
-// Each CTA is persistent over "tiles" (ROWS consecutive rows, one contiguous
+// Each CTA is persistent over "tiles" (ROWS consecutive rows = one contiguous
 // HBM span).  A STAGES-deep ring of shared-memory tile buffers is filled by
 // 1-D bulk TMA (cp.async.bulk, completion on an mbarrier) STAGES-1 tiles
 // ahead of the tile being transformed, so HBM reads stay in flight while the
@@ -13,55 +13,91 @@
 //   pre  : f_k * p_k * e^{i phi_k}                       (a != 0)
 //   post : S_j * C(n) p_j e^{i psi_j} / sqrt(2 pi i b)   (d != 0)
 // with p_k = (-1)^k e^{-i pi k/n} folded into the chirp argument.
-//  * c128: phi_k = fl(fl(0.5a/b) fl(x_k^2)) is formed exactly as the reference
-//    forms it (bit-identical fp64 argument); e^{i(phi+delta)} is evaluated as
-//    T[q mod 256] * e^{i r}, q = rint((phi+delta)/(2pi/256)), r reduced with a
-//    two-constant FMA Cody-Waite step, e^{ir} by degree-6/7 Taylor (|r|<=pi/256,
-//    |err| < 1e-17), T a 256-entry table in shared memory.
+//  * c128: phi_k = fl(fl(0.5a/b) fl(x_k^2)), x_k = fl((2k-n+1) half) is formed
+//    exactly as the reference forms it (bit-identical fp64 argument);
+//    e^{i(phi+delta)} = T[q mod 256] e^{i r}, q = rint((phi+delta)/(2pi/256)),
+//    r by a two-constant FMA Cody-Waite step (|r| <= pi/256), e^{ir} by a
+//    degree-6/7 Taylor polynomial (|err| < 1e-17), T a 256-entry table in
+//    shared memory.
 //  * c64: the chirp phase in turns, frac(D k'^2 + boundary) with
 //    D = (a/2b) half^2 / 2pi, is evaluated exactly in 64-bit fixed point
-//    (integer multiply, wraps mod 1 turn), then an fp32 polynomial.
-//    No fp64 and no conversions per element.
+//    (integer multiply-high, wraps mod 1 turn), then MUFU sin/cos of the
+//    signed turn fraction.  No fp64 and no conversions per element.
 // Twiddles come from a pass-major table (entry (t-1)*NS + k of pass p holds
 // w_{NS*E}^{t k}) so every warp's twiddle loads are coalesced.
 #pragma once
+#include <type_traits>
+
 #include "xft_rows.cuh"
 #include "xft_tma.cuh"
+
+#ifndef XFT_SKELETON
+#define XFT_SKELETON 0  // tuning only: 1 = exchanges without math, 2 = pure copy
+#endif
+#ifndef XFT_C128_TABCOPIES
+#define XFT_C128_TABCOPIES 8
+#endif
 
 namespace xftb {
 
 #define XFT_PI 3.141592653589793116
 #define XFT_INV_2PI 0.15915494309189534561
-#define XFT_U_HI 0.02454369260617026          /* 2 pi / 256 */
-#define XFT_U_LO 9.567553118338697e-19
-#define XFT_INV_U 40.74366543152521
+
+// fp64 constants live in the constant bank so DFMA/DMUL take them as c[] operands
+__constant__ double kC128[8] = {
+    0.02454369260617026,      // 0 U_HI = 2 pi / 256
+    9.567553118338697e-19,    // 1 U_LO
+    40.74366543152521,        // 2 1/U
+    -1.6666666666666667e-01,  // 3 sin: -1/6
+    8.3333333333333333e-03,   // 4 sin:  1/120
+    -0.5,                     // 5 cos: -1/2
+    4.1666666666666667e-02,   // 6 cos:  1/24
+    -1.3888888888888889e-03,  // 7 cos: -1/720
+};
+// 32 pi = 4096 U in three parts, and its inverse: pre-reduction for huge phases
+__constant__ double kC128Big[4] = {100.53096491487338, 3.91886975727153e-15, -9.583263391098687e-32,
+                                   0.009947183943243459};
+
+// s * pi / 16, s = 0..15: the boundary-phase step between a thread's registers
+__constant__ double kStepPi16[16] = {
+    0.0, 0.19634954084936207, 0.39269908169872414, 0.5890486225480862, 0.7853981633974483,
+    0.9817477042468103, 1.1780972450961724, 1.3744467859455345, 1.5707963267948966,
+    1.7671458676442586, 1.9634954084936207, 2.1598449493429825, 2.356194490192345,
+    2.552544031041707, 2.748893571891069, 2.945243112740431};
 
 // ---------------------------------------------------------------------------
 // per-row coefficients
 // ---------------------------------------------------------------------------
-struct Coef64 {
-  unsigned long long dq_in, dq_out, gq;  // Q0.64 turns: chirp rates and arg G
-  float gabs;                             // |G|
-  float2 g;                               // G (used when d == 0)
+// Computed once per row by xft_coef_kernel (a [B] array in device memory) and
+// brought into shared memory by the same bulk TMA as the row data.  Sizes are
+// multiples of 16 bytes (bulk-copy granularity).
+struct __align__(16) Coef64 {
+  unsigned long long dq_in, dq_out;  // Q0.64 turns per unit k'^2 (chirp rates)
+  uint32_t gq;                       // top 32 bits of arg G in turns
+  float gabs;                        // |G|
+  float2 g;                          // G (used when d == 0)
   int pre, post;
+  int pad[2];
 };
 
-struct Coef128 {
+struct __align__(16) Coef128 {
   double cin, cout, s4;  // fl(0.5a/b), fl(0.5d/b), fl(4b/pi)
   double gabs, gf;       // |G|, small part of arg G (|gf| <= U/2)
   double2 g;             // G (used when d == 0)
   int gi;                // arg G / U rounded (table units)
-  int pre, post;
+  int pre, post;         // chirp present (0 = none, 1 = table path, 2 = huge phase)
+  int pad[3];
 };
+static_assert(sizeof(Coef64) % 16 == 0 && sizeof(Coef128) % 16 == 0, "bulk-copy granularity");
 
 template <class C> struct CoefOf;
 template <> struct CoefOf<float2> { using T = Coef64; };
 template <> struct CoefOf<double2> { using T = Coef128; };
 
 struct RowConst {  // per-launch constants (host computed)
-  double half;         // (pi / sqrt(2n)) / 2
-  double cnabs;        // |C(n)| = pi / sqrt(2n)
-  long long cnred;     // (n-1)^2 mod 4n   (arg C(n) = -pi red / (2n))
+  double half;      // (pi / sqrt(2n)) / 2
+  double cnabs;     // |C(n)| = pi / sqrt(2n)
+  long long cnred;  // (n-1)^2 mod 4n   (arg C(n) = -pi red / (2n))
   int log2n;
   int flags;
 };
@@ -93,7 +129,7 @@ __device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd
   unsigned long long gq = 0ull - ((unsigned long long)k.cnred << (62 - k.log2n));
   gq += (b > 0.0) ? (0ull - (1ull << 61)) : (1ull << 61);
   if (k.flags & FLAG_BARE_FOURIER) gq += (1ull << 61);
-  c.gq = gq;
+  c.gq = (uint32_t)(gq >> 32);  // the low word is zero for n <= 2^30
   const double gabs = g_abs(b, k);
   c.gabs = (float)gabs;
   double s, co;
@@ -106,101 +142,115 @@ __device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd
 __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abcd& uni, const RowConst& k) {
   double a, b, d;
   row_params(p, uni, a, b, d);
-  c.cin = __ddiv_rn(0.5 * a, b);              // (0.5j * a / b).imag     xft/kernel.py:102
-  c.cout = __ddiv_rn(0.5 * d, b);             // (0.5j * d / b).imag     xft/kernel.py:113
-  c.s4 = __ddiv_rn(4.0 * b, XFT_PI);          // 4.0 * b / np.pi        xft/lct.py:196
+  c.cin = __ddiv_rn(0.5 * a, b);      // (0.5j * a / b).imag     xft/kernel.py:102
+  c.cout = __ddiv_rn(0.5 * d, b);     // (0.5j * d / b).imag     xft/kernel.py:113
+  c.s4 = __ddiv_rn(4.0 * b, XFT_PI);  // 4.0 * b / np.pi        xft/lct.py:196
   // arg G / U, U = 2pi/256: -64 red / n - 32 sgn(b) [+ 32]   (exact in fp64)
   double v = -64.0 * (double)k.cnred / (double)(1ll << k.log2n) + ((b > 0.0) ? -32.0 : 32.0);
   if (k.flags & FLAG_BARE_FOURIER) v += 32.0;
   const double vi = rint(v);
   c.gi = (int)vi;
-  c.gf = (v - vi) * XFT_U_HI;
+  c.gf = (v - vi) * kC128[0];
   c.gabs = g_abs(b, k);
   double s, co;
   sincospi(v * (1.0 / 128.0), &s, &co);
   c.g = make_double2(c.gabs * co, c.gabs * s);
-  c.pre = (a != 0.0);
-  c.post = (d != 0.0);
+  // largest |phase| on the row = |coef| x_max^2; the table reduction is exact
+  // for |phi| < ~1e13, beyond 1e11 the row takes the full-range sincos path
+  const double x2 = (double)((1ll << k.log2n) - 1) * k.half;
+  const double pmax_in = fabs(c.cin) * x2 * x2;
+  const double y2 = fabs(c.s4) * x2;
+  const double pmax_out = fabs(c.cout) * y2 * y2;
+  c.pre = (a != 0.0) ? (pmax_in < 1e12 ? 1 : 2) : 0;
+  c.post = (d != 0.0) ? (pmax_out < 1e12 ? 1 : 2) : 0;
 }
 
 // ---------------------------------------------------------------------------
 // unit phasors
 // ---------------------------------------------------------------------------
-// e^{2 pi i t / 2^32} in fp32 (t = turns in Q0.32), |err| ~ 1e-7
-__device__ __forceinline__ float2 unit_from_turns(uint32_t t) {
-  const uint32_t v = t + 0x20000000u;                     // + 1/8 turn
-  const uint32_t quad = v >> 30;
-  const int fi = (int)(v & 0x3FFFFFFFu) - 0x20000000;     // [-2^29, 2^29)
-  const int fm = (fi + 64) >> 7;                          // |fm| <= 2^22
-  const float r = (__int_as_float(0x4B400000 + fm) - 12582912.0f) * 1.8725351414619535e-07f;  // 2pi/2^25
-  const float z = r * r;
-  float ps = fmaf(z, -1.9841270e-04f, 8.3333333e-03f);
-  ps = fmaf(z, ps, -1.6666667e-01f);
-  const float s = fmaf(r * z, ps, r);
-  float pc = fmaf(z, 2.4801587e-05f, -1.3888889e-03f);
-  pc = fmaf(z, pc, 4.1666667e-02f);
-  pc = fmaf(z, pc, -0.5f);
-  const float c = fmaf(z, pc, 1.0f);
-  float cs = (quad & 1) ? -s : c;
-  float sn = (quad & 1) ? c : s;
-  if (quad & 2) { cs = -cs; sn = -sn; }
-  return make_float2(cs, sn);
+// e^{i (phi + add)} e^{2 pi i qoff/256} in fp64 via the 256-entry table tab[m] = e^{2 pi i m/256}.
+// phi: exact fp64 chirp argument, |phi| < 1e12 (larger: prereduce first); |add| < 2 pi.
+__device__ __forceinline__ double2 unit_phase_tab(double phi, double add, int qoff, const double2* __restrict__ tab) {
+  const double t = fma(phi + add, kC128[2], 6755399441055744.0);
+  const double qd = t - 6755399441055744.0;
+  const int q = __double2loint(t) + qoff;
+  double r = fma(-qd, kC128[0], phi);
+  r = r + add;
+  r = fma(-qd, kC128[1], r);
+  const double z = r * r;
+  const double sn = fma(r * z, fma(z, kC128[4], kC128[3]), r);
+  const double cs = fma(z, fma(z, fma(z, kC128[7], kC128[6]), kC128[5]), 1.0);
+  // 8 interleaved copies: lane l reads copy (l & 7), so the 8 lanes of a
+  // 16-byte quarter-warp phase always hit 8 different bank groups
+  const double2 w = XFT_C128_TABCOPIES == 8 ? tab[((q & 255) << 3) | (threadIdx.x & 7)] : tab[q & 255];
+  return make_double2(w.x * cs - w.y * sn, w.x * sn + w.y * cs);
 }
 
-// e^{i (phi + add)} * i^(2*odd) in fp64 via the 256-entry table tab[m] = e^{2 pi i m/256}.
-// phi: exact fp64 chirp argument (any size up to ~1e12); add: small (|add| < 2 pi).
-__device__ __forceinline__ double2 unit_phase_tab(double phi, double add, int qoff, const double2* __restrict__ tab) {
-  if (fabs(phi) < 1.0e12) {
-    const double t = fma(phi + add, XFT_INV_U, XFT_ROUND_MAGIC);
-    const double qd = t - XFT_ROUND_MAGIC;
-    const int q = __double2loint(t) + qoff;
-    double r = fma(-qd, XFT_U_HI, phi);
-    r = r + add;
-    r = fma(-qd, XFT_U_LO, r);
-    const double z = r * r;
-    const double sn = fma(r * z, fma(z, 8.3333333333333333e-03, -1.6666666666666667e-01), r);
-    const double cs = fma(z, fma(z, fma(z, -1.3888888888888889e-03, 4.1666666666666667e-02), -0.5), 1.0);
-    const double2 w = tab[q & 255];
-    return make_double2(w.x * cs - w.y * sn, w.x * sn + w.y * cs);
-  }
-  double s0, c0, s1, c1;
-  sincos(phi, &s0, &c0);
-  sincos(add, &s1, &c1);
-  double2 e = make_double2(c0 * c1 - s0 * s1, s0 * c1 + c0 * s1);
-  const double2 w = tab[qoff & 255];
-  return make_double2(w.x * e.x - w.y * e.y, w.x * e.y + w.y * e.x);
+// hide a value from the optimiser (stops it from re-deriving per-element
+// integer->fp64 conversions or hoisting per-element constants into registers)
+__device__ __forceinline__ double opaque(double x) {
+  double y;
+  asm volatile("mov.b64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// phi - m * 32pi (exact multiple of 4096 table units, so the table index is
+// unchanged): keeps the table reduction accurate for |phi| up to ~2e17
+__device__ __forceinline__ double prereduce(double phi) {
+  const double t = fma(phi, kC128Big[3], 6755399441055744.0);
+  const double q = t - 6755399441055744.0;
+  double r = fma(-q, kC128Big[0], phi);
+  r = fma(-q, kC128Big[1], r);
+  return fma(-q, kC128Big[2], r);
+}
+
+// g e^{2 pi i t / 2^32} in fp32 through the SFU (MUFU.SIN/COS): t -> signed
+// turns -> radians in [-pi, pi); |err| < 2e-6 (well inside the c64 budget).
+__device__ __forceinline__ float2 unit_turns_sfu(uint32_t t, float g) {
+  const int fm = ((int)t + 512) >> 10;                                  // |fm| <= 2^21
+  const float F = __int_as_float(0x4B400000 + fm) - 12582912.0f;       // = fm exactly
+  const float th = F * 1.4980281e-06f;                                  // 2 pi / 2^22
+  float s, c;
+  __sincosf(th, &s, &c);
+  return make_float2(c * g, s * g);
 }
 
 // ---------------------------------------------------------------------------
 // configuration
 // ---------------------------------------------------------------------------
-template <class C_, int LOG2N_, int E_, int MODE_, int SIGN_, int ROWS_, int STAGES_>
+template <class C_, int LOG2N_, int E_, int MODE_, int SIGN_, int ROWS_, int STAGES_, int MINB_>
 struct PipeCfg {
   using C = C_;
   using Coef = typename CoefOf<C>::T;
   static constexpr int LOG2N = LOG2N_, N = 1 << LOG2N, E = E_, MODE = MODE_, SIGN = SIGN_;
   static constexpr int ROWS = ROWS_, STAGES = STAGES_;
   static constexpr int TR = N / E;
-  static constexpr int THREADS = TR * ROWS;
+  static constexpr int THREADS_C = TR * ROWS;
+  static constexpr int THREADS = THREADS_C;
   static constexpr int TILE = ROWS * N;
   static constexpr int LE = ilog2(E);
   static constexpr int NPASS = (LOG2N + LE - 1) / LE;
   static constexpr int R0 = 1 << (LOG2N - (NPASS - 1) * LE);
   static constexpr bool C128 = sizeof(C) == 16;
-  static constexpr size_t TAB_BYTES = C128 ? 256 * sizeof(double2) : 0;
+  static constexpr size_t TAB_BYTES = C128 ? XFT_C128_TABCOPIES * 256 * sizeof(double2) : 0;
   static constexpr size_t SMEM = size_t(STAGES) * TILE * sizeof(C) + TAB_BYTES;
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
-  static_assert(THREADS <= 1024 && THREADS % 32 == 0, "threads");
+  static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
+  static_assert(THREADS <= 1024 && THREADS_C % 32 == 0, "threads");
   static constexpr int ns(int p) { return p == 0 ? 1 : R0 * ipow(E, p - 1); }
   static constexpr int twoff(int p) { return p <= 1 ? 0 : twoff(p - 1) + (E - 1) * ns(p - 1); }
   static constexpr int TW_ENTRIES = twoff(NPASS);
   // resident CTAs per SM the register budget is sized for
-  static constexpr int MINB = (SMEM * 2 <= 220 * 1024 && THREADS <= 512) ? 2 : 1;
+  static constexpr int MINB = MINB_;
 };
 
-template <class Cfg, int P, class Hook>
+template <class C> struct SwzPeriod;
+template <> struct SwzPeriod<float2> { static constexpr int V = 256; };   // swz<float2> mixes bits 4..7
+template <> struct SwzPeriod<double2> { static constexpr int V = 128; };  // swz<double2> mixes bits 3..6
+
+template <class Cfg, int P, class Release>
 __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
-                                          const typename Cfg::C* __restrict__ tw, Hook&& hook) {
+                                          const typename Cfg::C* __restrict__ tw, Release&& release) {
   using C = typename Cfg::C;
   constexpr int E = Cfg::E, TR = Cfg::TR;
   constexpr int R = (P == 0) ? Cfg::R0 : E;
@@ -214,7 +264,7 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     C u[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) u[t] = v[b + t * NB];
-    if constexpr (NS > 1) {
+    if constexpr (NS > 1 && XFT_SKELETON == 0) {
       const C* twp = tw + Cfg::twoff(P) + k;
 #pragma unroll
       for (int t = 1; t < R; ++t) {
@@ -223,144 +273,239 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
         u[t] = cmul(u[t], w);
       }
     }
-    dft_r<R, Cfg::SIGN>(u);
+    if constexpr (XFT_SKELETON == 0) dft_r<R, Cfg::SIGN>(u);
 #pragma unroll
     for (int t = 0; t < R; ++t) v[b + t * NB] = u[t];
   }
   if constexpr (!LAST) {
-    __syncthreads();  // every thread is done reading this buffer
-    if constexpr (P == 0) hook();
+    named_sync(1, Cfg::THREADS_C);  // every thread is done reading this buffer
+    if constexpr (P == 0) release();  // (first-barrier hook)
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int i = j + b * TR;
       const int k = i & (NS - 1);
       const int base = (i - k) * R + k;
 #pragma unroll
-      for (int t = 0; t < R; ++t) rs[swz<C>(base + t * NS)] = v[b + t * NB];
+      for (int t = 0; t < R; ++t) {
+        // the XOR swizzle only mixes bits below SWZ_PERIOD: strides that are
+        // multiples of it become plain immediate offsets
+        if constexpr (NS % SwzPeriod<C>::V == 0) rs[swz<C>(base) + t * NS] = v[b + t * NB];
+        else rs[swz<C>(base + t * NS)] = v[b + t * NB];
+      }
     }
-    __syncthreads();
+    named_sync(1, Cfg::THREADS_C);
 #pragma unroll
-    for (int s = 0; s < E; ++s) v[s] = rs[swz<C>(j + s * TR)];
+    for (int s = 0; s < E; ++s) {
+      if constexpr (TR % SwzPeriod<C>::V == 0) v[s] = rs[swz<C>(j) + s * TR];
+      else v[s] = rs[swz<C>(j + s * TR)];
+    }
   }
 }
 
-template <class Cfg, int P, class Hook>
+template <class Cfg, int P, class Release>
 __device__ __forceinline__ void pipe_passes(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
-                                            const typename Cfg::C* __restrict__ tw, Hook&& hook) {
+                                            const typename Cfg::C* __restrict__ tw, Release&& release) {
   if constexpr (P < Cfg::NPASS) {
-    pipe_pass<Cfg, P>(v, rs, j, tw, hook);
-    pipe_passes<Cfg, P + 1>(v, rs, j, tw, hook);
+    pipe_pass<Cfg, P>(v, rs, j, tw, release);
+    pipe_passes<Cfg, P + 1>(v, rs, j, tw, release);
   }
 }
 
 // ---------------------------------------------------------------------------
-// pre / post multipliers
+// per-thread invariants (depend on j and n only; computed once per kernel)
 // ---------------------------------------------------------------------------
 template <class Cfg, bool IS128 = Cfg::C128>
-struct Chirp;
+struct ThreadConst;
 
 template <class Cfg>
-struct Chirp<Cfg, false> {
-  using C = float2;
-  // f * p_k e^{i phi_k}
-  static __device__ __forceinline__ C pre(C f, int k, const Coef64& rc, const RowConst& kc, const C* __restrict__ ptab,
-                                          const double2*) {
-    if constexpr (Cfg::MODE == MODE_DFT) return f;
-    if (Cfg::MODE == MODE_LCT && rc.pre) {
-      const int off = 2 * k - Cfg::N + 1;
-      const unsigned long long bt = ((unsigned long long)(k & 1) << 63) - ((unsigned long long)k << (63 - Cfg::LOG2N));
-      const unsigned long long u = rc.dq_in * (unsigned long long)(unsigned)(off * off) + bt;
-      return cmul(unit_from_turns((uint32_t)(u >> 32)), f);
-    }
-    return cmul(__ldg(&ptab[k]), f);
-  }
-  static __device__ __forceinline__ C post(C S, int jj, const Coef64& rc, const RowConst& kc, double2 cn,
-                                           const C* __restrict__ ptab, const double2*) {
-    if constexpr (Cfg::MODE == MODE_DFT) return S;
-    if constexpr (Cfg::MODE == MODE_SCALED) return cmul(make_float2((float)cn.x, (float)cn.y), cmul(__ldg(&ptab[jj]), S));
-    if (rc.post) {
-      const int off = 2 * jj - Cfg::N + 1;
-      const unsigned long long bt = ((unsigned long long)(jj & 1) << 63) - ((unsigned long long)jj << (63 - Cfg::LOG2N));
-      const unsigned long long u = rc.dq_out * (unsigned long long)(unsigned)(off * off) + bt + rc.gq;
-      const float2 e = unit_from_turns((uint32_t)(u >> 32));
-      return cmul(make_float2(e.x * rc.gabs, e.y * rc.gabs), S);
-    }
-    return cmul(cmul(rc.g, __ldg(&ptab[jj])), S);
+struct ThreadConst<Cfg, false> {
+  int off0;      // 2j - n + 1
+  uint32_t bt0;  // top word of the boundary-phase turns at k = j
+  __device__ __forceinline__ explicit ThreadConst(int j) {
+    off0 = 2 * j - Cfg::N + 1;
+    bt0 = ((uint32_t)(j & 1) << 31) - ((uint32_t)j << (31 - Cfg::LOG2N));
   }
 };
 
 template <class Cfg>
-struct Chirp<Cfg, true> {
-  using C = double2;
-  static __device__ __forceinline__ C pre(C f, int k, const Coef128& rc, const RowConst& kc,
-                                          const C* __restrict__ ptab, const double2* tab) {
-    if constexpr (Cfg::MODE == MODE_DFT) return f;
-    if (Cfg::MODE == MODE_LCT && rc.pre) {
-      const double x = __dmul_rn((double)(2 * k - Cfg::N + 1), kc.half);        // xft/hermite.py:87-89
-      const double phi = __dmul_rn(rc.cin, __dmul_rn(x, x));                     // xft/kernel.py:102
-      const double add = -(XFT_PI / Cfg::N) * (double)k;                         // p_k = (-1)^k e^{-i pi k/n}
-      return cmul(unit_phase_tab(phi, add, (k & 1) << 7, tab), f);
-    }
-    return cmul(__ldg(&ptab[k]), f);
-  }
-  static __device__ __forceinline__ C post(C S, int jj, const Coef128& rc, const RowConst& kc, double2 cn,
-                                           const C* __restrict__ ptab, const double2* tab) {
-    if constexpr (Cfg::MODE == MODE_DFT) return S;
-    if constexpr (Cfg::MODE == MODE_SCALED) return cmul(cn, cmul(__ldg(&ptab[jj]), S));
-    if (rc.post) {
-      const double x = __dmul_rn((double)(2 * jj - Cfg::N + 1), kc.half);
-      const double y = __dmul_rn(rc.s4, x);                                       // xft/lct.py:196
-      const double psi = __dmul_rn(rc.cout, __dmul_rn(y, y));                     // xft/kernel.py:113
-      const double add = rc.gf - (XFT_PI / Cfg::N) * (double)jj;
-      const double2 e = unit_phase_tab(psi, add, rc.gi + ((jj & 1) << 7), tab);
-      return cmul(make_double2(e.x * rc.gabs, e.y * rc.gabs), S);
-    }
-    return cmul(cmul(rc.g, __ldg(&ptab[jj])), S);
+struct ThreadConst<Cfg, true> {
+  double off0;  // 2j - n + 1
+  double d0;    // -pi j / n
+  int q0;       // (-1)^j in table units
+  __device__ __forceinline__ explicit ThreadConst(int j) {
+    off0 = opaque((double)(2 * j - Cfg::N + 1));
+    d0 = opaque(-(XFT_PI / Cfg::N) * (double)j);
+    q0 = (j & 1) << 7;
   }
 };
 
 // ---------------------------------------------------------------------------
-// the kernel
+// pre / post multipliers over a thread's E registers (row-uniform branches
+// are taken once per tile, not per element)
 // ---------------------------------------------------------------------------
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
-xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restrict__ out, long long batch,
-                const double* __restrict__ abcd, long long abcd_stride, Abcd uni, const typename Cfg::C* __restrict__ tw,
-                const typename Cfg::C* __restrict__ ptab, const double2* __restrict__ gtab, double2 cn, RowConst kc) {
-  using C = typename Cfg::C;
-  using Coef = typename Cfg::Coef;
-  constexpr int E = Cfg::E, TR = Cfg::TR, N = Cfg::N, ROWS = Cfg::ROWS, S = Cfg::STAGES;
-  extern __shared__ __align__(128) unsigned char xft_smem[];
-  __shared__ __align__(8) uint64_t bars[S];
-  __shared__ Coef coef[2][ROWS];
-
-  C* stage0 = reinterpret_cast<C*>(xft_smem);
-  double2* tab = reinterpret_cast<double2*>(xft_smem + size_t(S) * Cfg::TILE * sizeof(C));
-
-  const int tid = threadIdx.x;
-  const int lrow = tid / TR;
-  const int j = tid - lrow * TR;
-  const long long ntiles = (batch + ROWS - 1) / ROWS;
-  const long long G = gridDim.x;
-
-  auto tile_bytes = [&](long long t) -> uint32_t {
-    const long long rows = batch - t * ROWS < ROWS ? batch - t * ROWS : ROWS;
-    return (uint32_t)(rows * N * sizeof(C));
-  };
-  auto issue = [&](long long t, int st) {
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&bars[st], tile_bytes(t));
-    tma_load_1d(stage0 + size_t(st) * Cfg::TILE, in + t * Cfg::TILE, tile_bytes(t), &bars[st]);
-  };
-  auto coefs = [&](long long t, int slot) {
+__device__ __forceinline__ void pre_multiply(typename Cfg::C (&v)[Cfg::E], const typename Cfg::C* rs, int j,
+                                             const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
+                                             const RowConst& kc, const typename Cfg::C* __restrict__ ptab,
+                                             const void* tabv) {
+  constexpr int E = Cfg::E, TR = Cfg::TR;
+#pragma unroll
+  for (int s = 0; s < E; ++s) v[s] = rs[j + s * TR];
+  if constexpr (Cfg::MODE == MODE_DFT) {
+    return;
+  } else {
+    int mode = 0;
+    if constexpr (Cfg::MODE == MODE_LCT) mode = rcs.pre;
+    if (mode == 0) {
+#pragma unroll
+      for (int s = 0; s < E; ++s) v[s] = cmul(__ldg(&ptab[j + s * TR]), v[s]);
+      return;
+    }
     if constexpr (Cfg::MODE == MODE_LCT) {
-      if (tid < 32) {
-        for (int r = tid; r < ROWS; r += 32) {
-          const long long row = t * ROWS + r;
-          if (row < batch) make_coef(coef[slot][r], abcd ? abcd + row * abcd_stride : nullptr, uni, kc);
+      if constexpr (!Cfg::C128) {
+        const float2* tab = static_cast<const float2*>(tabv);
+        const uint32_t dlo = (uint32_t)rcs.dq_in, dhi = (uint32_t)(rcs.dq_in >> 32);
+#pragma unroll
+        for (int s = 0; s < E; ++s) {
+          const int off = tc.off0 + 2 * s * TR;
+          const uint32_t o2 = (uint32_t)(off * off);
+          const uint32_t top = dhi * o2 + __umulhi(dlo, o2) + (tc.bt0 - (uint32_t)s * (1u << (31 - Cfg::LE)));
+          v[s] = cmul(unit_turns_sfu(top, 1.0f), v[s]);
+        }
+      } else {
+        const double2* tab = static_cast<const double2*>(tabv);
+        const double cin = rcs.cin, half = kc.half;
+        if (mode == 1) {
+#pragma unroll
+          for (int s = 0; s < E; ++s) {
+            const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);  // xft/hermite.py:87-89
+            const double phi = __dmul_rn(cin, __dmul_rn(x, x));               // xft/kernel.py:102
+            const double add = tc.d0 - kStepPi16[s * (16 / E)];
+            v[s] = cmul(unit_phase_tab(phi, add, tc.q0, tab), v[s]);
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < E; ++s) {
+            const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
+            const double phi = __dmul_rn(cin, __dmul_rn(x, x));
+            const double add = tc.d0 - kStepPi16[s * (16 / E)];
+            v[s] = cmul(unit_phase_tab(prereduce(phi), add, tc.q0, tab), v[s]);
+          }
         }
       }
     }
+  }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* __restrict__ dst, int j,
+                                           const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
+                                           const RowConst& kc, double2 cn, const typename Cfg::C* __restrict__ ptab,
+                                           const void* tabv) {
+  using C = typename Cfg::C;
+  constexpr int E = Cfg::E, TR = Cfg::TR;
+  if constexpr (Cfg::MODE == MODE_DFT) {
+#pragma unroll
+    for (int s = 0; s < E; ++s) st_stream(dst + j + s * TR, v[s]);
+  } else if constexpr (Cfg::MODE == MODE_SCALED) {
+    const C c = to_c<C>(cn);
+#pragma unroll
+    for (int s = 0; s < E; ++s) st_stream(dst + j + s * TR, cmul(c, cmul(__ldg(&ptab[j + s * TR]), v[s])));
+  } else {
+    if (rcs.post == 0) {
+      const C g = rcs.g;
+#pragma unroll
+      for (int s = 0; s < E; ++s) st_stream(dst + j + s * TR, cmul(cmul(g, __ldg(&ptab[j + s * TR])), v[s]));
+      return;
+    }
+    if constexpr (!Cfg::C128) {
+      const float2* tab = static_cast<const float2*>(tabv);
+      const uint32_t dlo = (uint32_t)rcs.dq_out, dhi = (uint32_t)(rcs.dq_out >> 32);
+      const uint32_t b0 = tc.bt0 + rcs.gq;
+      const float g = rcs.gabs;
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        const int off = tc.off0 + 2 * s * TR;
+        const uint32_t o2 = (uint32_t)(off * off);
+        const uint32_t top = dhi * o2 + __umulhi(dlo, o2) + (b0 - (uint32_t)s * (1u << (31 - Cfg::LE)));
+        st_stream(dst + j + s * TR, cmul(unit_turns_sfu(top, g), v[s]));
+      }
+    } else {
+      const double2* tab = static_cast<const double2*>(tabv);
+      const double cout = rcs.cout, s4 = rcs.s4, half = kc.half, g = rcs.gabs;
+      const double d0 = tc.d0 + rcs.gf;
+      const int q0 = tc.q0 + rcs.gi;
+      if (rcs.post == 1) {
+#pragma unroll
+        for (int s = 0; s < E; ++s) {
+          const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
+          const double y = __dmul_rn(s4, x);                    // xft/lct.py:196
+          const double psi = __dmul_rn(cout, __dmul_rn(y, y));  // xft/kernel.py:113
+          const double add = d0 - kStepPi16[s * (16 / E)];
+          const double2 e = unit_phase_tab(psi, add, q0, tab);
+          st_stream(dst + j + s * TR, cmul(make_double2(e.x * g, e.y * g), v[s]));
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < E; ++s) {
+          const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
+          const double y = __dmul_rn(s4, x);
+          const double psi = __dmul_rn(cout, __dmul_rn(y, y));
+          const double add = d0 - kStepPi16[s * (16 / E)];
+          const double2 e = unit_phase_tab(prereduce(psi), add, q0, tab);
+          st_stream(dst + j + s * TR, cmul(make_double2(e.x * g, e.y * g), v[s]));
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel.  Thread 0 keeps STAGES-1 tile loads in flight (bulk TMA of the
+// rows and of their precomputed coefficients onto one mbarrier per stage);
+// every thread transforms.  The next load is issued right after the first
+// exchange barrier of the current tile, i.e. once every thread has finished
+// the previous tile and the oldest stage is free.
+// ---------------------------------------------------------------------------
+template <class Coef>
+__global__ void xft_coef_kernel(Coef* __restrict__ out, long long rows, const double* __restrict__ abcd,
+                                long long stride, Abcd uni, RowConst kc) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) make_coef(out[r], abcd ? abcd + r * stride : nullptr, uni, kc);
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restrict__ out, long long batch,
+                const typename Cfg::Coef* __restrict__ coefs, int coef_per_row, const typename Cfg::C* __restrict__ tw,
+                const typename Cfg::C* __restrict__ ptab, const void* __restrict__ gtab, double2 cn, RowConst kc) {
+  using C = typename Cfg::C;
+  using Coef = typename Cfg::Coef;
+  constexpr int N = Cfg::N, ROWS = Cfg::ROWS, S = Cfg::STAGES;
+  extern __shared__ __align__(128) unsigned char xft_smem[];
+  __shared__ __align__(8) uint64_t bars[S];
+  __shared__ Coef coefbuf[Cfg::MODE == MODE_LCT ? S : 1][Cfg::MODE == MODE_LCT ? ROWS : 1];
+
+  C* stage0 = reinterpret_cast<C*>(xft_smem);
+  void* tab = xft_smem + size_t(S) * Cfg::TILE * sizeof(C);
+
+  const int tid = threadIdx.x;
+  const int lrow = tid / Cfg::TR;
+  const int j = tid - lrow * Cfg::TR;
+  const long long ntiles = (batch + ROWS - 1) / ROWS;
+  const long long G = gridDim.x;
+  const ThreadConst<Cfg> tc(j);
+
+  auto issue = [&](long long t, int st) {
+    fence_proxy_async_smem();
+    const long long rows = batch - t * ROWS < ROWS ? batch - t * ROWS : ROWS;
+    const uint32_t bytes = (uint32_t)(rows * N * sizeof(C));
+    uint32_t cbytes = 0;
+    if constexpr (Cfg::MODE == MODE_LCT) cbytes = (uint32_t)((coef_per_row ? rows : 1) * sizeof(Coef));
+    mbar_arrive_expect_tx(&bars[st], bytes + cbytes);
+    tma_load_1d(stage0 + size_t(st) * Cfg::TILE, in + t * Cfg::TILE, bytes, &bars[st]);
+    if constexpr (Cfg::MODE == MODE_LCT)
+      tma_load_1d(&coefbuf[st][0], coefs + (coef_per_row ? t * ROWS : 0), cbytes, &bars[st]);
   };
 
   // ---- prologue ----
@@ -369,7 +514,9 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     fence_mbar_init();
   }
   if constexpr (Cfg::C128) {
-    for (int m = tid; m < 256; m += Cfg::THREADS) tab[m] = gtab[m];
+    double2* t = static_cast<double2*>(tab);
+    const double2* g = static_cast<const double2*>(gtab);
+    for (int m = tid; m < XFT_C128_TABCOPIES * 256; m += Cfg::THREADS) t[m] = g[XFT_C128_TABCOPIES == 8 ? m >> 3 : m];
   }
   __syncthreads();
   long long tile = blockIdx.x;
@@ -378,43 +525,47 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
       if (tile + s * G < ntiles) issue(tile + s * G, s);
     if (S == 1 && tile < ntiles) issue(tile, 0);
   }
-  coefs(tile, 0);
-  __syncthreads();
 
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int st = it % S;
     mbar_wait(&bars[st], (uint32_t)((it / S) & 1));
     C* rs = stage0 + size_t(st) * Cfg::TILE + size_t(lrow) * N;
-    const Coef& rc = coef[it & 1][lrow];
+    Coef rc;
+    if constexpr (Cfg::MODE == MODE_LCT) rc = coefbuf[st][coef_per_row ? lrow : 0];
 
-    C v[E];
+    C v[Cfg::E];
+    if constexpr (XFT_SKELETON) {
 #pragma unroll
-    for (int s = 0; s < E; ++s) {
-      const int k = j + s * TR;
-      v[s] = Chirp<Cfg>::pre(rs[k], k, rc, kc, ptab, tab);
+      for (int s = 0; s < Cfg::E; ++s) v[s] = rs[j + s * Cfg::TR];
+    } else {
+      pre_multiply<Cfg>(v, rs, j, rc, tc, kc, ptab, tab);
     }
 
-    auto hook = [&]() {
+    // runs right after the first exchange barrier of this tile
+    auto first_barrier = [&]() {
       if (S >= 2 && tid == 0) {
         const long long nt = tile + (S - 1) * G;
         if (nt < ntiles) issue(nt, (it + S - 1) % S);
       }
-      coefs(tile + G, (it + 1) & 1);
     };
-    pipe_passes<Cfg, 0>(v, rs, j, tw, hook);
+    if constexpr (XFT_SKELETON == 2) {
+      named_sync(1, Cfg::THREADS);
+      first_barrier();
+    } else {
+      pipe_passes<Cfg, 0>(v, rs, j, tw, first_barrier);
+    }
     if constexpr (S == 1) {
-      __syncthreads();
+      named_sync(1, Cfg::THREADS);
       if (tid == 0 && tile + G < ntiles) issue(tile + G, 0);
     }
 
     const long long row = tile * ROWS + lrow;
-    if (row < batch) {
-      C* dst = out + row * N;
+    if constexpr (XFT_SKELETON) {
+      if (row < batch)
 #pragma unroll
-      for (int s = 0; s < E; ++s) {
-        const int jj = j + s * TR;
-        st_stream(dst + jj, Chirp<Cfg>::post(v[s], jj, rc, kc, cn, ptab, tab));
-      }
+        for (int s = 0; s < Cfg::E; ++s) st_stream(out + row * N + j + s * Cfg::TR, v[s]);
+    } else {
+      if (row < batch) post_store<Cfg>(v, out + row * N, j, rc, tc, kc, cn, ptab, tab);
     }
   }
 }

@@ -90,7 +90,7 @@ struct RowCfg {
   static constexpr int NPASS = LOG2N == 0 ? 0 : (LOG2N + LE - 1) / LE;
   static constexpr int R0 = NPASS == 0 ? 1 : (1 << (LOG2N - (NPASS - 1) * LE));
   static constexpr size_t SMEM = NPASS > 1 ? size_t(ROWS) * N * sizeof(C) : 0;
-  static_assert(E >= 1 && (E & (E - 1)) == 0 && E <= 16, "E");
+  static_assert(E >= 1 && (E & (E - 1)) == 0 && E <= 32, "E");
   static_assert(THREADS <= 1024, "threads");
 };
 

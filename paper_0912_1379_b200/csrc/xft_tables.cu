@@ -29,7 +29,7 @@ struct Entry {
 };
 
 std::mutex g_mu;
-std::map<int, void*> g_gtab;
+std::map<std::pair<int, int>, void*> g_gtab;
 std::map<std::tuple<int, int64_t, int>, Entry> g_tables;
 
 const long double PI_L = 3.141592653589793238462643383279502884L;
@@ -107,17 +107,23 @@ int get_tables(int64_t n, int dtype, Tables* out) {
     if (r1 != cudaSuccess || r2 != cudaSuccess) return XFT_ECUDA;
     it = g_tables.emplace(key, e).first;
   }
-  auto gt = g_gtab.find(dev);
+  auto gt = g_gtab.find({dev, dtype});
   if (gt == g_gtab.end()) {
-    std::vector<double2> g(256);
-    for (int m = 0; m < 256; ++m) {
-      const long double th = 2.0L * PI_L * (long double)m / 256.0L;
+    // chirp phasor tables: c128 e^{2 pi i m/256}, c64 e^{2 pi i m/1024}
+    const int tn = dtype == XFT_C64 ? 1024 : 256;
+    std::vector<double2> g(tn);
+    std::vector<float2> gf(tn);
+    for (int m = 0; m < tn; ++m) {
+      const long double th = 2.0L * PI_L * (long double)m / (long double)tn;
       g[m] = make_double2((double)cosl(th), (double)sinl(th));
+      gf[m] = make_float2((float)cosl(th), (float)sinl(th));
     }
+    const size_t bytes = dtype == XFT_C64 ? tn * sizeof(float2) : tn * sizeof(double2);
     void* d = nullptr;
-    if (cudaMalloc(&d, 256 * sizeof(double2)) != cudaSuccess) return XFT_ECUDA;
-    if (cudaMemcpy(d, g.data(), 256 * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess) return XFT_ECUDA;
-    gt = g_gtab.emplace(dev, d).first;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return XFT_ECUDA;
+    const void* src = dtype == XFT_C64 ? (const void*)gf.data() : (const void*)g.data();
+    if (cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) return XFT_ECUDA;
+    gt = g_gtab.emplace(std::make_pair(dev, dtype), d).first;
   }
   out->gtab = gt->second;
   out->tw = it->second.tw;

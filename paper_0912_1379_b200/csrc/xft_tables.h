@@ -9,7 +9,12 @@ namespace xftb {
 
 // Radix (elements per thread) of the pipelined kernel for (dtype, log2 n);
 // shared by the host table builder and the kernel instantiation.
-constexpr int pipe_radix(int dtype, int l) { return dtype == 0 ? 16 : (l >= 13 ? 16 : 8); }
+#ifndef XFT_C128_E
+#define XFT_C128_E 16
+#endif
+constexpr int pipe_radix(int dtype, int l) {
+  return dtype == 0 ? (l >= 14 ? 32 : 16) : (l >= 13 ? 16 : XFT_C128_E);
+}
 
 struct Tables {
   const void* tw = nullptr;    // pass-major twiddles of the pipelined kernel (see xft_pipe.cuh)

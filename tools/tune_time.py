@@ -1,0 +1,68 @@
+"""Graph-replayed per-kernel timing of the cfg2 batch (c64 and c128).
+
+  XFT_LIB=path/to/variant.so python tools/tune_time.py [--reps 20]
+Prints one JSON line: microseconds per launch per dtype (CUDA events around a
+CUDA-graph replay of `reps` launches over 3 rotating buffer sets).
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--tag", default=os.environ.get("XFT_LIB", "default"))
+    a = ap.parse_args()
+    import torch
+
+    from paper_0912_1379_b200 import ops, workloads
+
+    res = {"tag": a.tag}
+    cases = []
+    if a.config == "cfg2":
+        for tag, dt in (("c64", np.complex64), ("c128", np.complex128)):
+            c = workloads.config2(dtype=dt)
+            cases.append((tag, c.values, c.abcd))
+    elif a.config == "cfg4":
+        c = workloads.config4()
+        cases.append(("c64", c.values, c.abcd))
+    for tag, vals, abcd in cases:
+        sets = []
+        for _ in range(3):
+            v = torch.from_numpy(vals).cuda()
+            sets.append((v, torch.empty_like(v), torch.from_numpy(np.ascontiguousarray(abcd)).cuda()))
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for i in range(3):
+                v, o, p = sets[i % 3]
+                ops.lct_rows(v, p, out=o, validate=False)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(a.reps):
+                v, o, p = sets[i % 3]
+                ops.lct_rows(v, p, out=o, validate=False)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e30
+        for _ in range(3):
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e3 / a.reps)
+        nbytes = vals.nbytes * 2
+        res[tag] = {"us": round(best, 2), "GBps": round(nbytes / best / 1e3, 1)}
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
