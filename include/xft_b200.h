@@ -99,14 +99,15 @@ int xft_scaled_fourier(const void* in, void* out, int64_t batch, int64_t n, int 
 int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
                  int64_t abcd_stride, int flags, int check_unimodular, double tol);
 
-/* Complex-z fractional transform through the Mehler kernel (device pointers):
+/* Complex-z fractional transform through the Mehler kernel (in/out: device):
  *   out_j = dx sqrt(2/(1-z^2)) sum_k exp(-((1+z^2)(x_j^2+x_k^2) - 4 x_j x_k z) / (2(1-z^2))) in_k
  * i.e. frft_matrix_asymptotic(n, FrftOrder(z)).apply(in) (xft/dense.py:122-151,
- * 76-80) evaluated in O(n log n) as a Bluestein convolution.  z: device array
- * of batch (re, im) pairs (z_stride 2) or one pair (z_stride 0); |z| <= 1,
- * z != +-1 validated by the caller (xft_validate_mehler_z).  dtype C128 only
- * (the reference tolerance 1e-12 needs fp64).  `workspace` : device scratch of
- * xft_mehler_workspace_bytes(batch, n) bytes. */
+ * 76-80) evaluated in O(n log n) as a windowed Bluestein convolution.
+ * z: HOST array of batch (re, im) pairs (z_stride 2) or one pair (z_stride 0);
+ * it is validated here (|z| <= 1 + 1e-12, |z -+ 1| >= 1e-14: XFT_EPARAM /
+ * XFT_ESINGULAR, as FrftOrder / mehler_kernel).  complex128 only (the 1e-12
+ * tolerance needs fp64).  `workspace`: device scratch of
+ * xft_mehler_workspace_bytes(batch, n) bytes, or NULL to allocate on `stream`. */
 int64_t xft_mehler_workspace_bytes(int64_t batch, int64_t n);
 int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double* z, int64_t z_stride,
                void* workspace, void* stream);

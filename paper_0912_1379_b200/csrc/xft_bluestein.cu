@@ -1,0 +1,310 @@
+// Host side of the chirp-z kernels: arbitrary-length DFT / scaled Fourier /
+// LCT (xft/fftcore.py:84-100, 116-119) and the complex-z Mehler transform
+// (xft/dense.py:122-151).  Plan tables are built once per (device, n, sign,
+// dtype, mode) on the host in long double and cached (immutable).
+#include <array>
+#include <cmath>
+#include <complex>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "../../include/xft_b200.h"
+#include "xft_blue.cuh"
+#include "xft_internal.h"
+#include "xft_tables.h"
+
+using namespace xftb;
+
+namespace {
+
+using cld = std::complex<long double>;
+const long double PI_L = 3.141592653589793238462643383279502884L;
+
+constexpr int MAXL_C64 = 14;   // M <= 16384 (128 KiB exchange buffer)
+constexpr int MAXL_C128 = 13;  // M <= 8192
+
+// iterative radix-2 FFT, sign s (plan-time only)
+void host_fft(std::vector<cld>& a, int s) {
+  const size_t n = a.size();
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    const long double ang = s * 2.0L * PI_L / (long double)len;
+    for (size_t i = 0; i < n; i += len)
+      for (size_t k = 0; k < len / 2; ++k) {
+        const cld w(cosl(ang * k), sinl(ang * k));
+        const cld u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+  }
+}
+
+struct CzPlan {
+  double2* pre = nullptr;
+  double2* post = nullptr;
+  double2* hspec = nullptr;
+  int64_t m = 0;
+};
+
+std::mutex g_mu;
+std::map<std::tuple<int, int64_t, int, int>, CzPlan> g_plans;  // (dev, n, sign, mode)
+
+int get_plan(int64_t n, int sign, int mode, CzPlan* out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(dev, n, sign, mode);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) {
+    *out = it->second;
+    return XFT_OK;
+  }
+  int64_t m = 1;
+  while (m < 2 * n - 1) m *= 2;
+  // chirp_k = exp(s i pi (k^2 mod 2n) / n)           (xft/fftcore.py:88-90)
+  std::vector<cld> chirp(n), filt(m, cld(0, 0));
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t r = (int64_t)(((__int128)k * k) % (2 * (__int128)n));
+    const long double th = sign * PI_L * (long double)r / (long double)n;
+    chirp[k] = cld(cosl(th), sinl(th));
+  }
+  for (int64_t k = 0; k < n; ++k) filt[k] = std::conj(chirp[k]);  // xft/fftcore.py:91-93
+  for (int64_t k = 1; k < n; ++k) filt[m - k] = std::conj(chirp[k]);
+  host_fft(filt, -1);
+  std::vector<double2> pre(n), post(n), hs(m);
+  // C(n) and p_k for the scaled-Fourier / LCT wrappers (xft/kernel.py:45-65)
+  const int64_t red = (int64_t)(((__int128)(n - 1) * (n - 1)) % (4 * (__int128)n));
+  const cld cn = (PI_L / sqrtl(2.0L * n)) * cld(cosl(PI_L * red / (2.0L * n)), -sinl(PI_L * red / (2.0L * n)));
+  for (int64_t k = 0; k < n; ++k) {
+    cld a = chirp[k], b = chirp[k] / (long double)m;
+    if (mode != 0) {
+      const int64_t rk = (int64_t)(((__int128)(n - 1) * k) % (2 * (__int128)n));
+      const cld p(cosl(PI_L * rk / (long double)n), sinl(PI_L * rk / (long double)n));
+      a *= p;
+      b *= p * cn;
+    }
+    pre[k] = make_double2((double)a.real(), (double)a.imag());
+    post[k] = make_double2((double)b.real(), (double)b.imag());
+  }
+  for (int64_t k = 0; k < m; ++k) hs[k] = make_double2((double)filt[k].real(), (double)filt[k].imag());
+  CzPlan p;
+  p.m = m;
+  if (cudaMalloc(&p.pre, n * sizeof(double2)) != cudaSuccess) return XFT_ECUDA;
+  if (cudaMalloc(&p.post, n * sizeof(double2)) != cudaSuccess) return XFT_ECUDA;
+  if (cudaMalloc(&p.hspec, m * sizeof(double2)) != cudaSuccess) return XFT_ECUDA;
+  if (cudaMemcpy(p.pre, pre.data(), n * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p.post, post.data(), n * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p.hspec, hs.data(), m * sizeof(double2), cudaMemcpyHostToDevice) != cudaSuccess)
+    return XFT_ECUDA;
+  g_plans.emplace(key, p);
+  *out = p;
+  return XFT_OK;
+}
+
+template <class C, int L, class Op>
+int launch_blue(const void* in, void* out, long long rows, const int* rowlist, const Op& op, cudaStream_t st) {
+  if constexpr (L < 2) {
+    return XFT_ENOTSUP;
+  } else {
+    constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
+    constexpr int E = blue_radix(dtype, L);
+    using BC = BlueCfg<C, L, E>;
+    auto kern = xft_blue_kernel<C, L, E, Op>;
+    Tables tb;
+    int rc = get_tables(int64_t(1) << L, dtype, &tb, E);
+    if (rc) return rc;
+    if (BC::SMEM > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BC::SMEM) != cudaSuccess)
+      return XFT_ECUDA;
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC::TR, BC::SMEM);
+    const long long cap = (long long)sms * (occ < 1 ? 1 : (occ > 8 ? 8 : occ));  // Mehler scratch: <= 8 rows/SM
+    const long long grid = rows < cap ? rows : cap;
+    kern<<<(unsigned)grid, BC::TR, BC::SMEM, st>>>(static_cast<const C*>(in), static_cast<C*>(out), rows, rowlist, op,
+                                                   static_cast<const C*>(tb.tw));
+    return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+  }
+}
+
+template <class C, class Op, int... Ls>
+int dispatch_blue(int l, const void* in, void* out, long long rows, const int* rowlist, const Op& op,
+                  cudaStream_t st, std::integer_sequence<int, Ls...>) {
+  int rc = XFT_ENOTSUP;
+  ((l == Ls ? (rc = launch_blue<C, Ls, Op>(in, out, rows, rowlist, op, st), 0) : 0), ...);
+  return rc;
+}
+
+template <class C, class Op>
+int blue(int l, const void* in, void* out, long long rows, const int* rowlist, const Op& op, cudaStream_t st) {
+  constexpr int MAXL = sizeof(C) == 8 ? MAXL_C64 : MAXL_C128;
+  if (l < 2 || l > MAXL) return XFT_ENOTSUP;
+  return dispatch_blue<C, Op>(l, in, out, rows, rowlist, op, st, std::make_integer_sequence<int, MAXL + 1>{});
+}
+
+int log2_ceil(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+}  // namespace
+
+namespace xftb {
+
+int64_t chirpz_max_m(int dtype) { return int64_t(1) << (dtype == XFT_C64 ? MAXL_C64 : MAXL_C128); }
+
+int run_chirpz(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+               int64_t stride, const double* uni4, int flags, cudaStream_t st) {
+  if (n < 2) return XFT_EINVALID_SIZE;
+  int64_t m = 1;
+  while (m < 2 * n - 1) m *= 2;
+  if (m > chirpz_max_m(dtype)) return XFT_ENOTSUP;
+  CzPlan p;
+  int rc = get_plan(n, mode == 0 ? sign : -1, mode == 0 ? 0 : 1, &p);
+  if (rc) return rc;
+  OpChirpZ op;
+  op.pre = p.pre;
+  op.post = p.post;
+  op.hspec = p.hspec;
+  op.abcd = abcd;
+  op.abcd_stride = stride;
+  op.uni = uni4 ? Abcd{uni4[0], uni4[1], uni4[2], uni4[3]} : Abcd{0, 0, 0, 0};
+  op.half = host_half_step(n);
+  op.n = (int)n;
+  op.lct = mode == 2;
+  op.bare = (flags & XFT_FLAG_BARE_FOURIER) ? 1 : 0;
+  const int l = log2_ceil(m);
+  return dtype == XFT_C64 ? blue<float2>(l, in, out, batch, nullptr, op, st)
+                          : blue<double2>(l, in, out, batch, nullptr, op, st);
+}
+
+}  // namespace xftb
+
+// ---------------------------------------------------------------------------
+// Mehler (complex-z fractional transform)
+// ---------------------------------------------------------------------------
+namespace {
+
+struct MehlerPlanRow {
+  OpMehlerRow p;
+  int l;
+};
+
+MehlerPlanRow mehler_row(std::complex<double> z, int64_t n) {
+  using cd = std::complex<double>;
+  const double half = host_half_step(n);
+  const cd one = 1.0 - z * z;
+  const cd A = std::sqrt(2.0 / one);                     // principal branch, xft/dense.py:135
+  const cd Q = 2.0 * z / one;
+  const int sigma = Q.real() >= 0.0 ? 1 : -1;
+  // gamma' = P - sigma Q/2 in closed form (no cancellation near z = +-1)
+  const cd gam = sigma > 0 ? (1.0 - z) / (2.0 * (1.0 + z)) : (1.0 + z) / (2.0 * (1.0 - z));
+  const cd beta = 2.0 * (double)sigma * Q * half * half;  // h(l) = exp(-beta l^2)
+  // window: keep samples with exp(-Re(gam) x^2) > 1e-20 (|x| < sqrt(46 / Re gam))
+  int64_t k0 = 0;
+  if (gam.real() > 0.0) {
+    const double xc = std::sqrt(46.0 / gam.real());
+    const double kk = std::ceil(xc / (2.0 * half)) + 1.0;
+    if (kk < n / 2) k0 = n / 2 - (int64_t)kk;
+  }
+  const int64_t wn = n - 2 * k0;
+  int64_t m = 1;
+  while (m < 2 * wn - 1) m *= 2;
+  if (m < 4) m = 4;
+  const cd scale = (2.0 * half) * A / (double)m;
+  MehlerPlanRow r;
+  r.p.gam = make_double2(gam.real(), gam.imag());
+  r.p.beta = make_double2(beta.real(), beta.imag());
+  r.p.scale = make_double2(scale.real(), scale.imag());
+  r.p.k0 = (int)k0;
+  r.p.wn = (int)wn;
+  r.p.sigma = sigma;
+  r.p.pad = 0;
+  r.l = log2_ceil(m);
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t xft_mehler_workspace_bytes(int64_t batch, int64_t n) {
+  // per resident CTA one kernel-spectrum row of the largest class + the row tables
+  int64_t m = 1;
+  while (m < 2 * n - 1) m *= 2;
+  return (int64_t)148 * 8 * m * 16 + batch * (int64_t)(sizeof(OpMehlerRow) + sizeof(int)) + 4096;
+}
+
+int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double* z, int64_t z_stride,
+               void* workspace, void* stream) {
+  if (n < 1 || batch < 0) return XFT_EINVALID_SIZE;
+  int rc = xft_validate_mehler_z(z, batch, z_stride, nullptr);
+  if (rc) return rc;
+  if (batch == 0) return XFT_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  // per-row parameters and size classes
+  std::vector<MehlerPlanRow> pr(batch);
+  std::map<int, std::vector<int>> classes;
+  for (int64_t r = 0; r < batch; ++r) {
+    const double* zz = z + (z_stride ? r * z_stride : 0);
+    pr[r] = mehler_row(std::complex<double>(zz[0], zz[1]), n);
+    classes[pr[r].l].push_back((int)r);
+  }
+  for (auto& kv : classes)
+    if (kv.first > MAXL_C128) return XFT_ENOTSUP;  // window longer than the in-CTA limit (n > 4096 with z near +-1)
+  std::vector<OpMehlerRow> rows(batch);
+  for (int64_t r = 0; r < batch; ++r) rows[r] = pr[r].p;
+  std::vector<int> order;
+  order.reserve(batch);
+  for (auto& kv : classes) order.insert(order.end(), kv.second.begin(), kv.second.end());
+  // device scratch: row table, row lists, one kernel-spectrum row per launched CTA
+  const int maxl = classes.rbegin()->first;
+  const size_t tab_bytes = (size_t)batch * sizeof(OpMehlerRow);
+  const size_t list_bytes = ((size_t)batch * sizeof(int) + 255) & ~size_t(255);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << maxl) * sizeof(double2);
+  char* ws = static_cast<char*>(workspace);
+  bool own = false;
+  const size_t need = ((tab_bytes + 255) & ~size_t(255)) + list_bytes + hs_bytes;
+  if (!ws) {
+    if (cudaMallocAsync((void**)&ws, need, st) != cudaSuccess) return XFT_ECUDA;
+    own = true;
+  }
+  OpMehlerRow* d_rows = reinterpret_cast<OpMehlerRow*>(ws);
+  int* d_list = reinterpret_cast<int*>(ws + ((tab_bytes + 255) & ~size_t(255)));
+  double2* d_hs = reinterpret_cast<double2*>(ws + ((tab_bytes + 255) & ~size_t(255)) + list_bytes);
+  if (cudaMemcpyAsync(d_rows, rows.data(), tab_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(d_list, order.data(), batch * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    if (own) cudaFreeAsync(ws, st);
+    return XFT_ECUDA;
+  }
+  OpMehler op;
+  op.rows = d_rows;
+  op.hscratch = d_hs;
+  op.half = host_half_step(n);
+  op.n = (int)n;
+  size_t off = 0;
+  for (auto& kv : classes) {
+    const long long cnt = (long long)kv.second.size();
+    rc = blue<double2>(kv.first, in, out, cnt, d_list + off, op, st);
+    if (rc) break;
+    off += cnt;
+  }
+  if (own) cudaFreeAsync(ws, st);
+  // (the pageable host vectors above were staged by cudaMemcpyAsync before it returned)
+  return rc;
+}
+
+}  // extern "C"

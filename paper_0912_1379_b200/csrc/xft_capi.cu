@@ -7,6 +7,7 @@
 
 #include "../../include/xft_b200.h"
 #include "xft_pipe.cuh"
+#include "xft_internal.h"
 #include "xft_tables.h"
 
 using namespace xftb;
@@ -158,9 +159,13 @@ int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64
   if (n < 1) return XFT_EINVALID_SIZE;
   if (batch < 0) return XFT_EINVALID_SIZE;
   if (dtype != XFT_C64 && dtype != XFT_C128) return XFT_EPARAM;
-  const int l = log2_exact(n);
-  if (l < 0 || l > (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128)) return XFT_ENOTSUP;
   if (batch == 0) return XFT_OK;
+  const int l = log2_exact(n);
+  if (l < 0) {  // not a power of two: chirp-z route (xft/fftcore.py:84-100)
+    const double u4[4] = {uni.a, uni.b, uni.c, uni.d};
+    return run_chirpz(mode, sign, in, out, batch, n, dtype, abcd, stride, u4, flags, st);
+  }
+  if (l > (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128)) return XFT_ENOTSUP;
   LaunchArgs a{in, out, (long long)batch, abcd, (long long)stride, uni, {}, flags, st};
   int rc = get_tables(n, dtype, &a.tb);
   if (rc) return rc;
@@ -221,7 +226,8 @@ int64_t xft_max_n(int dtype) { return int64_t(1) << (dtype == XFT_C64 ? MAXLOG_C
 
 int xft_prepare(int64_t n, int dtype) {
   if (n < 1) return XFT_EINVALID_SIZE;
-  if (log2_exact(n) < 0 || n > xft_max_n(dtype)) return XFT_ENOTSUP;
+  if (log2_exact(n) < 0) return XFT_OK;  // chirp-z plans are built on first use
+  if (n > xft_max_n(dtype)) return XFT_ENOTSUP;
   Tables tb;
   return get_tables(n, dtype, &tb);
 }
@@ -302,7 +308,7 @@ int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype,
                  int64_t abcd_stride, int flags, int check_unimodular, double tol) {
   if (n < 1 || batch < 0) return XFT_EINVALID_SIZE;
   if (dtype != XFT_C64 && dtype != XFT_C128) return XFT_EPARAM;
-  if (log2_exact(n) < 0 || n > xft_max_n(dtype)) return XFT_ENOTSUP;
+  if (log2_exact(n) >= 0 && n > xft_max_n(dtype)) return XFT_ENOTSUP;
   int rc = xft_validate_lct_params(abcd, batch, abcd_stride, check_unimodular, tol, nullptr);
   if (rc) return rc;
   if (batch == 0) return XFT_OK;
@@ -362,7 +368,6 @@ int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype,
   return rc;
 }
 
-int64_t xft_mehler_workspace_bytes(int64_t batch, int64_t n) { return 0; }
 
 int xft_validate_mehler_z(const double* z, int64_t count, int64_t stride, int64_t* bad_row) {
   const int64_t rows = stride == 0 ? (count > 0 ? 1 : 0) : count;
@@ -380,6 +385,5 @@ int xft_validate_mehler_z(const double* z, int64_t count, int64_t stride, int64_
   return XFT_OK;
 }
 
-int xft_mehler(const void*, void*, int64_t, int64_t, const double*, int64_t, void*, void*) { return XFT_ENOTSUP; }
 
 }  // extern "C"

@@ -283,12 +283,12 @@ template <int SIGN, class C> __device__ __forceinline__ void dft16(C* v) {
 }
 
 // w32^k (k = 1..15), cos and sin of 2 pi k / 32
-__constant__ const double kW32c[16] = {1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452,
+static __constant__ const double kW32c[16] = {1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452,
                                        0.7071067811865476, 0.5555702330196023, 0.38268343236508984,
                                        0.19509032201612833, 0.0, -0.19509032201612833, -0.38268343236508984,
                                        -0.5555702330196023, -0.7071067811865476, -0.8314696123025452,
                                        -0.9238795325112867, -0.9807852804032304};
-__constant__ const double kW32s[16] = {0.0, 0.19509032201612825, 0.3826834323650898, 0.5555702330196022,
+static __constant__ const double kW32s[16] = {0.0, 0.19509032201612825, 0.3826834323650898, 0.5555702330196022,
                                        0.7071067811865475, 0.8314696123025452, 0.9238795325112867,
                                        0.9807852804032304, 1.0, 0.9807852804032304, 0.9238795325112867,
                                        0.8314696123025452, 0.7071067811865475, 0.5555702330196022,

@@ -1,0 +1,18 @@
+// Internal entry points shared between the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace xftb {
+
+struct Abcd;
+
+// chirp-z route for lengths that are not powers of two (xft_bluestein.cu);
+// mode: 0 DFT (sign), 1 scaled Fourier, 2 LCT.  abcd: device, stride 0|4.
+int run_chirpz(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+               int64_t stride, const double* uni4, int flags, cudaStream_t st);
+
+// largest M (power of two) the in-CTA chirp-z kernel handles for dtype
+int64_t chirpz_max_m(int dtype);
+
+}  // namespace xftb

@@ -44,7 +44,7 @@ namespace xftb {
 #define XFT_INV_2PI 0.15915494309189534561
 
 // fp64 constants live in the constant bank so DFMA/DMUL take them as c[] operands
-__constant__ double kC128[8] = {
+static __constant__ double kC128[8] = {
     0.02454369260617026,      // 0 U_HI = 2 pi / 256
     9.567553118338697e-19,    // 1 U_LO
     40.74366543152521,        // 2 1/U
@@ -55,11 +55,11 @@ __constant__ double kC128[8] = {
     -1.3888888888888889e-03,  // 7 cos: -1/720
 };
 // 32 pi = 4096 U in three parts, and its inverse: pre-reduction for huge phases
-__constant__ double kC128Big[4] = {100.53096491487338, 3.91886975727153e-15, -9.583263391098687e-32,
+static __constant__ double kC128Big[4] = {100.53096491487338, 3.91886975727153e-15, -9.583263391098687e-32,
                                    0.009947183943243459};
 
 // s * pi / 16, s = 0..15: the boundary-phase step between a thread's registers
-__constant__ double kStepPi16[16] = {
+static __constant__ double kStepPi16[16] = {
     0.0, 0.19634954084936207, 0.39269908169872414, 0.5890486225480862, 0.7853981633974483,
     0.9817477042468103, 1.1780972450961724, 1.3744467859455345, 1.5707963267948966,
     1.7671458676442586, 1.9634954084936207, 2.1598449493429825, 2.356194490192345,
@@ -236,7 +236,7 @@ struct PipeCfg {
   static constexpr size_t SMEM = size_t(STAGES) * TILE * sizeof(C) + TAB_BYTES;
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
-  static_assert(THREADS <= 1024 && THREADS_C % 32 == 0, "threads");
+  static_assert(THREADS <= 1024, "threads");
   static constexpr int ns(int p) { return p == 0 ? 1 : R0 * ipow(E, p - 1); }
   static constexpr int twoff(int p) { return p <= 1 ? 0 : twoff(p - 1) + (E - 1) * ns(p - 1); }
   static constexpr int TW_ENTRIES = twoff(NPASS);
@@ -278,7 +278,7 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     for (int t = 0; t < R; ++t) v[b + t * NB] = u[t];
   }
   if constexpr (!LAST) {
-    named_sync(1, Cfg::THREADS_C);  // every thread is done reading this buffer
+    __syncthreads();  // every thread is done reading this buffer
     if constexpr (P == 0) release();  // (first-barrier hook)
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -293,7 +293,7 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
         else rs[swz<C>(base + t * NS)] = v[b + t * NB];
       }
     }
-    named_sync(1, Cfg::THREADS_C);
+    __syncthreads();
 #pragma unroll
     for (int s = 0; s < E; ++s) {
       if constexpr (TR % SwzPeriod<C>::V == 0) v[s] = rs[swz<C>(j) + s * TR];
@@ -549,13 +549,13 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
       }
     };
     if constexpr (XFT_SKELETON == 2) {
-      named_sync(1, Cfg::THREADS);
+      __syncthreads();
       first_barrier();
     } else {
       pipe_passes<Cfg, 0>(v, rs, j, tw, first_barrier);
     }
     if constexpr (S == 1) {
-      named_sync(1, Cfg::THREADS);
+      __syncthreads();
       if (tid == 0 && tile + G < ntiles) issue(tile + G, 0);
     }
 

@@ -155,7 +155,7 @@ xft_rows_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
                 const typename Cfg::C* __restrict__ ptab, double2 cn, double half, int flags) {
   using C = typename Cfg::C;
   constexpr int E = Cfg::E, TR = Cfg::TR, N = Cfg::N, ROWS = Cfg::ROWS;
-  extern __shared__ __align__(16) unsigned char xft_smem[];
+  extern __shared__ __align__(128) unsigned char xft_smem[];
   __shared__ RowCoef coef[Cfg::MODE == MODE_LCT ? ROWS : 1];
 
   const int tid = threadIdx.x;

@@ -30,7 +30,7 @@ struct Entry {
 
 std::mutex g_mu;
 std::map<std::pair<int, int>, void*> g_gtab;
-std::map<std::tuple<int, int64_t, int>, Entry> g_tables;
+std::map<std::tuple<int, int64_t, int, int>, Entry> g_tables;
 
 const long double PI_L = 3.141592653589793238462643383279502884L;
 
@@ -71,19 +71,19 @@ void fill(std::vector<T2>& pt, int64_t n) {
 
 }  // namespace
 
-int get_tables(int64_t n, int dtype, Tables* out) {
+int get_tables(int64_t n, int dtype, Tables* out, int radix) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
   out->cn = host_kernel_prefactor(n);
   out->half = host_half_step(n);
   std::lock_guard<std::mutex> lk(g_mu);
-  auto key = std::make_tuple(dev, n, dtype);
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  const int E = radix > 0 ? radix : pipe_radix(dtype, l);
+  auto key = std::make_tuple(dev, n, dtype, E);
   auto it = g_tables.find(key);
   if (it == g_tables.end()) {
     Entry e;
-    int l = 0;
-    while ((int64_t(1) << l) < n) ++l;
-    const int E = pipe_radix(dtype, l);
     cudaError_t r1 = cudaSuccess, r2 = cudaSuccess;
     auto upload = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
       if (bytes == 0) bytes = 16;  // keep a valid pointer for empty tables

@@ -25,7 +25,12 @@ struct Tables {
 };
 
 // Returns 0 and fills *out, or an XFT_E* status.  Thread-safe.
-int get_tables(int64_t n, int dtype, Tables* out);
+int get_tables(int64_t n, int dtype, Tables* out, int radix = -1);
+
+// radix of the in-CTA chirp-z kernels for an FFT of length 2^l
+constexpr int blue_radix(int dtype, int l) {
+  return pipe_radix(dtype, l) < (1 << (l - 1)) ? pipe_radix(dtype, l) : (1 << (l - 1));
+}
 
 // Host formulas shared with the C-ABI.
 double2 host_kernel_prefactor(int64_t n);

@@ -1,0 +1,144 @@
+"""GPU parity for the chirp-z kernels: non-power-of-two lengths and the Mehler transform."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import xft_oracle as O
+from tests.conftest import max_row_rel_l2, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+
+    if not _t.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return _t
+
+
+@pytest.fixture(scope="module")
+def X():
+    import paper_0912_1379_b200 as X
+
+    return X
+
+
+def dev(torch, a, dtype=None):
+    a = np.asarray(a)
+    if dtype is not None:
+        a = a.astype(dtype)
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+NONPOW2 = [3, 5, 6, 7, 9, 10, 11, 12, 13, 15, 17, 20, 24, 31, 37, 100, 384, 600, 1000]
+
+
+@pytest.mark.parametrize("n", NONPOW2)
+def test_chirpz_dft_golden(torch, X, golden, n):
+    v = golden[f"dft_in_n{n}"]
+    for sign in (1, -1):
+        plan = X.plan_dft(n, sign)
+        assert plan.route == "chirp-z"
+        got = X.apply_dft(plan, v)
+        assert rel_l2(got, golden[f"dft_out_n{n}_s{sign}"]) <= 1e-12, (n, sign)
+        got64 = X.ops.dft_rows(dev(torch, v[None], np.complex64), sign).cpu().numpy()[0]
+        ref64 = O.dft_rows(v.astype(np.complex64).astype(complex), sign)
+        assert rel_l2(got64, ref64) <= 2e-5, (n, sign)
+
+
+def test_chirpz_batched_and_naive(torch, X):
+    rng = np.random.default_rng(7)
+    for n in (3, 96, 1000, 4095):
+        v = rng.normal(size=(5, n)) + 1j * rng.normal(size=(5, n))
+        got = X.ops.dft_rows(dev(torch, v), -1).cpu().numpy()
+        ref = O.dft_rows(v, -1) if n > 1000 else O.naive_dft(v, -1)
+        assert max_row_rel_l2(got, ref) <= 1e-11, n
+
+
+@pytest.mark.parametrize("n", [7, 1000])
+def test_chirpz_scaled_fourier_golden(torch, X, golden, n):
+    got = X.apply_scaled_fourier(golden[f"sf_in_n{n}"])
+    assert rel_l2(got, golden[f"sf_out_n{n}"]) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [3, 5, 6, 7, 100, 1000])
+def test_chirpz_lct_golden(torch, X, golden, n):
+    f = golden[f"lct_in_n{n}"]
+    P = golden[f"lct_abcd_n{n}"]
+    got = X.ops.lct_rows(dev(torch, np.broadcast_to(f, (P.shape[0], n))), P).cpu().numpy()
+    assert max_row_rel_l2(got, golden[f"lct_out_n{n}"]) <= 1e-12
+    got64 = X.ops.lct_rows(dev(torch, np.broadcast_to(f, (P.shape[0], n)), np.complex64), P).cpu().numpy()
+    _, ref64 = O.fast_lct_rows(P, np.broadcast_to(f, (P.shape[0], n)).astype(np.complex64).astype(complex))
+    assert max_row_rel_l2(got64, ref64) <= 2e-5
+
+
+def test_chirpz_fourier_frft_n96(torch, X, golden):
+    g = X.Signal(X.asymptotic_zeros(96), golden["fourier_in_n96"])
+    assert rel_l2(X.xft_fourier(g).values, golden["fourier_out_n96"]) <= 1e-12
+    for t, ref in zip((0.3, math.pi / 2, -0.7, 3.0), golden["frft_out_n96"]):
+        assert rel_l2(X.fast_frft(t, g).values, ref) <= 1e-12
+
+
+def test_norm_scaling_nonpow2(torch, X):
+    # pkg/tests/test_lct.py:146-159 analogue: ||G||^2 = pi/(4|b|) ||f||^2
+    rng = np.random.default_rng(7)
+    for n in (7, 1000):
+        f = rng.normal(size=n) + 1j * rng.normal(size=n)
+        res = X.fast_lct(X.LctParams(1.0, 2.0, 0.5, 2.0), X.Signal(X.asymptotic_zeros(n), f))
+        lhs = np.sum(np.abs(res.values) ** 2)
+        rhs = math.pi / 8 * np.sum(np.abs(f) ** 2)
+        assert abs(lhs - rhs) <= 1e-10 * rhs
+
+
+# --------------------------------------------------------------------------
+# Mehler (complex z) -- frft_matrix_asymptotic semantics
+# --------------------------------------------------------------------------
+def _mehler_tol(z):
+    # the reference's own expo loses ~|x|^2 / |1-z^2| ulps near z = +-1
+    return 2e-12 if abs(1 - z * z) < 0.05 else 1e-12
+
+
+@pytest.mark.parametrize("n", [2, 8, 64, 256, 1024, 4096])
+def test_mehler_golden(torch, X, golden, n):
+    f = golden[f"mehler_in_n{n}"]
+    zs = golden[f"mehler_z_n{n}"]
+    got = X.mehler_rows(dev(torch, np.broadcast_to(f, (zs.shape[0], n))), zs).cpu().numpy()
+    for g, ref, z in zip(got, golden[f"mehler_out_n{n}"], zs):
+        assert rel_l2(g, ref) <= _mehler_tol(z), (n, z)
+    # the drop-in object: frft_matrix_asymptotic(n, FrftOrder(z)).apply(v)
+    z = zs[2]
+    got1 = X.frft_matrix_asymptotic(n, X.FrftOrder(z)).apply(f)
+    assert rel_l2(got1, golden[f"mehler_out_n{n}"][2]) <= 1e-12
+
+
+def test_mehler_config3_rows_at_dense_cap(torch, X, golden):
+    got = X.mehler_rows(dev(torch, golden["cfg3s_in"]), golden["cfg3s_z"]).cpu().numpy()
+    for g, ref, z in zip(got, golden["cfg3s_out"], golden["cfg3s_z"]):
+        assert rel_l2(g, ref) <= _mehler_tol(z)
+
+
+def test_mehler_errors(torch, X):
+    v = dev(torch, np.ones((1, 16), dtype=complex))
+    with pytest.raises(X.ParameterError):
+        X.FrftOrder(1.1)
+    with pytest.raises(X.SingularParameterError):
+        X.mehler_rows(v, 1.0)
+    with pytest.raises(X.SingularParameterError):
+        X.frft_matrix_asymptotic(8, X.FrftOrder(-1.0))
+    with pytest.raises(X.ParameterError):
+        X.mehler_rows(v.to(torch.complex64), 0.5)
+
+
+def test_mehler_hermite_eigen(torch, X):
+    # continuum limit: K_z psi_m ~ sqrt(2 pi) z^m psi_m (SURVEY 8(c) closed forms)
+    n = 1024
+    x = X.asymptotic_zeros(n).nodes
+    psi = X.hermite_function_table(8, x)
+    z = 0.6 * np.exp(0.7j)
+    got = X.mehler_rows(dev(torch, psi.astype(complex)), z).cpu().numpy()
+    for m in range(8):
+        ref = math.sqrt(2 * math.pi) * z ** m * psi[m]
+        assert rel_l2(got[m], ref) <= 1e-10, m
