@@ -260,15 +260,15 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
     pr[r] = mehler_row(std::complex<double>(zz[0], zz[1]), n);
     classes[pr[r].l].push_back((int)r);
   }
-  for (auto& kv : classes)
-    if (kv.first > MAXL_C128) return XFT_ENOTSUP;  // window longer than the in-CTA limit (n > 4096 with z near +-1)
   std::vector<OpMehlerRow> rows(batch);
   for (int64_t r = 0; r < batch; ++r) rows[r] = pr[r].p;
   std::vector<int> order;
   order.reserve(batch);
   for (auto& kv : classes) order.insert(order.end(), kv.second.begin(), kv.second.end());
   // device scratch: row table, row lists, one kernel-spectrum row per launched CTA
-  const int maxl = classes.rbegin()->first;
+  int maxl = 0;  // largest class served by the in-CTA kernel (scratch sizing)
+  for (auto& kv : classes)
+    if (kv.first <= MAXL_C128) maxl = kv.first;
   const size_t tab_bytes = (size_t)batch * sizeof(OpMehlerRow);
   const size_t list_bytes = ((size_t)batch * sizeof(int) + 255) & ~size_t(255);
   int dev = 0, sms = 0;
@@ -298,7 +298,8 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
   size_t off = 0;
   for (auto& kv : classes) {
     const long long cnt = (long long)kv.second.size();
-    rc = blue<double2>(kv.first, in, out, cnt, d_list + off, op, st);
+    rc = kv.first <= MAXL_C128 ? blue<double2>(kv.first, in, out, cnt, d_list + off, op, st)
+                               : run_large_mehler(in, out, cnt, d_list + off, d_rows, kv.first, n, st);
     if (rc) break;
     off += cnt;
   }

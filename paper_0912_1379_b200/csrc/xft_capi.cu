@@ -165,7 +165,10 @@ int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64
     const double u4[4] = {uni.a, uni.b, uni.c, uni.d};
     return run_chirpz(mode, sign, in, out, batch, n, dtype, abcd, stride, u4, flags, st);
   }
-  if (l > (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128)) return XFT_ENOTSUP;
+  if (l > (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128)) {  // longer than one CTA: four-step path
+    const double u4[4] = {uni.a, uni.b, uni.c, uni.d};
+    return run_large_pow2(mode, sign, in, out, batch, n, dtype, abcd, stride, u4, flags, st);
+  }
   LaunchArgs a{in, out, (long long)batch, abcd, (long long)stride, uni, {}, flags, st};
   int rc = get_tables(n, dtype, &a.tb);
   if (rc) return rc;
@@ -222,12 +225,13 @@ extern "C" {
 
 int xft_version(void) { return 100; }
 
-int64_t xft_max_n(int dtype) { return int64_t(1) << (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128); }
+int64_t xft_max_n(int dtype) { return int64_t(1) << 20; }  // four-step path beyond the in-CTA sizes
 
 int xft_prepare(int64_t n, int dtype) {
   if (n < 1) return XFT_EINVALID_SIZE;
   if (log2_exact(n) < 0) return XFT_OK;  // chirp-z plans are built on first use
   if (n > xft_max_n(dtype)) return XFT_ENOTSUP;
+  if (n > (int64_t(1) << (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128))) return XFT_OK;  // four-step: built on use
   Tables tb;
   return get_tables(n, dtype, &tb);
 }

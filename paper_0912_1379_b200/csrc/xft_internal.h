@@ -15,4 +15,11 @@ int run_chirpz(int mode, int sign, const void* in, void* out, int64_t batch, int
 // largest M (power of two) the in-CTA chirp-z kernel handles for dtype
 int64_t chirpz_max_m(int dtype);
 
+// four-step path (xft_large.cu) for rows longer than the in-CTA kernels
+int run_large_pow2(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype,
+                   const double* abcd, int64_t stride, const double* uni4, int flags, cudaStream_t st);
+struct OpMehlerRow;
+int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm, int l,
+                     int64_t n, cudaStream_t st);
+
 }  // namespace xftb

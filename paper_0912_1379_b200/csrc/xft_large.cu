@@ -1,0 +1,572 @@
+// Four-step path for rows longer than one CTA (M = M1 * M2 > in-CTA limit).
+//
+//   X[k1 + M1 k2] = sum_m2 w_M^{k1 m2} w_M2^{k2 m2} [ sum_m1 x[m1 M2 + m2] w_M1^{k1 m1} ]
+//
+// pass 1 ("columns"): length-M1 DFTs down the columns of the [M1][M2] view,
+//          fused with the input generator / pre-multiplier and the w_M^{k1 m2}
+//          twiddle, result in place ([k1][m2]);
+// pass 2 ("rows"):    length-M2 DFTs along the rows.  Its store either goes to
+//          natural order (transposed, coalesced in W-wide chunks) fused with the
+//          post-multiplier, or stays permuted ([k1][k2]) for a convolution.
+// Convolutions (chirp-z, Mehler) keep the spectrum permuted: the row pass
+// multiplies by the permuted kernel spectrum between a forward and an inverse
+// FFT, applies the conjugate twiddle, and an inverse column pass returns to
+// natural order fused with the post-multiplier.  Scratch lives in device
+// memory (L2-resident for the configurations of BASELINE.json).
+#include <cmath>
+#include <complex>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "../../include/xft_b200.h"
+#include "xft_blue.cuh"
+#include "xft_internal.h"
+#include "xft_tables.h"
+#include "xft_tile.cuh"
+
+using namespace xftb;
+
+namespace {
+
+const long double PI_L = 3.141592653589793238462643383279502884L;
+
+template <class C> constexpr int tile_w() { return sizeof(C) == 8 ? 16 : 8; }    // 128-byte lines
+template <class C> constexpr int tile_e(int l) { return l >= 8 ? (sizeof(C) == 8 ? 16 : 8) : 8; }
+
+// natural twiddles e^{-2 pi i m / M}, m < M, per (device, M, dtype)
+std::mutex g_mu;
+std::map<std::tuple<int, int64_t, int>, void*> g_nat;
+
+int natural_twiddles(int64_t M, int dtype, const void** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(dev, M, dtype);
+  auto it = g_nat.find(key);
+  if (it == g_nat.end()) {
+    const size_t esz = dtype == XFT_C64 ? 8 : 16;
+    std::vector<double2> d(M);
+    std::vector<float2> f(M);
+    for (int64_t m = 0; m < M; ++m) {
+      const long double th = 2.0L * PI_L * (long double)m / (long double)M;
+      d[m] = make_double2((double)cosl(th), (double)-sinl(th));
+      f[m] = make_float2((float)cosl(th), (float)-sinl(th));
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, esz * M) != cudaSuccess) return XFT_ECUDA;
+    if (cudaMemcpy(p, dtype == XFT_C64 ? (const void*)f.data() : (const void*)d.data(), esz * M,
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+      return XFT_ECUDA;
+    it = g_nat.emplace(key, p).first;
+  }
+  *out = it->second;
+  return XFT_OK;
+}
+
+struct Shape {
+  int l1, l2;  // M1 = 2^l1 (columns pass), M2 = 2^l2 (rows pass)
+  long long M;
+};
+Shape split(int l) {
+  Shape s;
+  s.l1 = (l + 1) / 2;
+  s.l2 = l / 2;
+  s.M = 1ll << l;
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// generators / pre-multipliers of pass 1 (natural index m of row b)
+// ---------------------------------------------------------------------------
+template <class C>
+struct GenLoad {  // plain input row
+  const C* in;
+  const int* rowlist;
+  long long M;
+  __device__ C operator()(long long b, long long m) const {
+    const long long row = rowlist ? rowlist[b] : b;
+    return in[row * M + m];
+  }
+};
+
+struct RowChirp {  // exact LCT chirp coefficients + row factor (per row)
+  double cin, cout, s4;
+  double2 g;
+  int pre, post;
+  int pad[2];
+};
+
+template <class C>
+struct GenLct {  // x p_k e^{i phi_k}  (pow2 n = M), or just p_k (scaled Fourier)
+  const C* in;
+  const RowChirp* rc;
+  const double2* ptab;  // p_k, natural
+  double half;
+  long long n;
+  int lct;
+  __device__ C operator()(long long b, long long k) const {
+    double2 u = cmul_d(ptab[k], to_d2(in[b * n + k]));
+    if (lct && rc[b].pre) {
+      const double x = __dmul_rn((double)(2 * k - n + 1), half);
+      const double phi = __dmul_rn(rc[b].cin, __dmul_rn(x, x));
+      double s, c;
+      sincos(phi, &s, &c);
+      u = cmul_d(make_double2(c, s), u);
+    }
+    return to_c<C>(u);
+  }
+};
+
+template <class C>
+struct GenChirpZ {  // chirp-z: pre[k] x [e^{i phi_k}] for k < n, zero padding beyond
+  const C* in;
+  const RowChirp* rc;
+  const double2* pre;
+  double half;
+  long long n;
+  int lct;
+  __device__ C operator()(long long b, long long k) const {
+    if (k >= n) return to_c<C>(make_double2(0.0, 0.0));
+    double2 u = cmul_d(pre[k], to_d2(in[b * n + k]));
+    if (lct && rc[b].pre) {
+      const double x = __dmul_rn((double)(2 * k - n + 1), half);
+      const double phi = __dmul_rn(rc[b].cin, __dmul_rn(x, x));
+      double s, c;
+      sincos(phi, &s, &c);
+      u = cmul_d(make_double2(c, s), u);
+    }
+    return to_c<C>(u);
+  }
+};
+
+struct GenMehlerH {  // kernel h(lag) = exp(-beta lag^2), circular lags
+  const OpMehlerRow* rows;
+  const int* rowlist;
+  long long M;
+  __device__ double2 operator()(long long b, long long m) const {
+    const OpMehlerRow p = rows[rowlist[b]];
+    const long long lag = m < p.wn ? m : (m > M - p.wn ? m - M : -(1ll << 62));
+    if (lag == -(1ll << 62)) return make_double2(0.0, 0.0);
+    const double l2 = (double)lag * (double)lag;
+    return cexp_d(-p.beta.x * l2, -p.beta.y * l2);
+  }
+};
+
+struct GenMehlerU {  // windowed input times exp(-gam x^2)
+  const double2* in;
+  const OpMehlerRow* rows;
+  const int* rowlist;
+  double half;
+  long long n;
+  __device__ double2 operator()(long long b, long long m) const {
+    const long long row = rowlist[b];
+    const OpMehlerRow p = rows[row];
+    if (m >= p.wn) return make_double2(0.0, 0.0);
+    const long long k = p.k0 + m;
+    const long long ks = p.sigma > 0 ? k : n - 1 - k;
+    const double x = (double)(2 * k - n + 1) * half;
+    const double x2 = x * x;
+    return cmul_d(cexp_d(-p.gam.x * x2, -p.gam.y * x2), in[row * n + ks]);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// pass operators
+// ---------------------------------------------------------------------------
+template <class C, class Gen>
+struct OpCols {  // pass 1: columns (generator in, twiddled permuted-column out)
+  static constexpr bool MID = false;
+  Gen gen;
+  C* out;
+  const C* twm;  // natural twiddles of length M
+  int M2, W;
+  long long M;
+  int conj_tw;   // +1 transforms use the conjugate twiddle
+  __device__ C load(long long tile, int w, int a) const {
+    const int cb = M2 / W;
+    const long long b = tile / cb;
+    const int c = (int)(tile % cb) * W + w;
+    return gen(b, (long long)a * M2 + c);
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    const int cb = M2 / W;
+    const long long b = tile / cb;
+    const int c = (int)(tile % cb) * W + w;
+    const C w8 = twm[(long long)a * c];
+    out[b * M + (long long)a * M2 + c] = cmul(v, conj_tw ? cconj(w8) : w8);
+  }
+};
+
+template <class C, class Post>
+struct OpRowsNat {  // pass 2 of a plain FFT: rows, transposed store to natural order
+  static constexpr bool MID = false;
+  const C* scr;
+  Post post;
+  int M1, M2, W;
+  long long M;
+  __device__ C load(long long tile, int w, int a) const {
+    const int rb = M1 / W;
+    const long long b = tile / rb;
+    const int k1 = (int)(tile % rb) * W + w;
+    return scr[b * M + (long long)k1 * M2 + a];
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    const int rb = M1 / W;
+    const long long b = tile / rb;
+    const int k1 = (int)(tile % rb) * W + w;
+    post(b, k1 + (long long)M1 * a, v);
+  }
+};
+
+template <class C>
+struct OpRowsPerm {  // pass 2 kept permuted (kernel spectra)
+  static constexpr bool MID = false;
+  C* scr;
+  int M1, M2, W;
+  long long M;
+  __device__ C load(long long tile, int w, int a) const {
+    const long long b = tile / (M1 / W);
+    const int k1 = (int)(tile % (M1 / W)) * W + w;
+    return scr[b * M + (long long)k1 * M2 + a];
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    const long long b = tile / (M1 / W);
+    const int k1 = (int)(tile % (M1 / W)) * W + w;
+    scr[b * M + (long long)k1 * M2 + a] = v;
+  }
+};
+
+template <class C>
+struct OpRowsConv {  // rows: forward, x spectrum, inverse, conjugate twiddle
+  static constexpr bool MID = true;
+  C* scr;
+  const C* spec;  // permuted spectrum, row stride spec_stride (0: shared by all rows)
+  long long spec_stride;
+  const C* twm;
+  int M1, M2, W;
+  long long M;
+  __device__ long long base(long long tile, int w, int& k1) const {
+    const long long b = tile / (M1 / W);
+    k1 = (int)(tile % (M1 / W)) * W + w;
+    return b;
+  }
+  __device__ C load(long long tile, int w, int a) const {
+    int k1;
+    const long long b = base(tile, w, k1);
+    return scr[b * M + (long long)k1 * M2 + a];
+  }
+  __device__ C mid(long long tile, int w, int a, C v) const {
+    int k1;
+    const long long b = base(tile, w, k1);
+    return cmul(v, spec[b * spec_stride + (long long)k1 * M2 + a]);
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    int k1;
+    const long long b = base(tile, w, k1);
+    scr[b * M + (long long)k1 * M2 + a] = cmul(v, cconj(twm[(long long)k1 * a]));
+  }
+};
+
+template <class C, class Post>
+struct OpColsInv {  // inverse columns: permuted [k1][m2] -> natural m = m1 M2 + m2, fused post
+  static constexpr bool MID = false;
+  const C* scr;
+  Post post;
+  int M2, W;
+  long long M;
+  __device__ C load(long long tile, int w, int a) const {
+    const long long b = tile / (M2 / W);
+    const int c = (int)(tile % (M2 / W)) * W + w;
+    return scr[b * M + (long long)a * M2 + c];
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    const long long b = tile / (M2 / W);
+    const int c = (int)(tile % (M2 / W)) * W + w;
+    post(b, (long long)a * M2 + c, v);
+  }
+};
+
+// post-multipliers (natural output index j of row b)
+template <class C>
+struct PostLct {
+  C* out;
+  const RowChirp* rc;
+  const double2* post;  // C(n) p_j (LCT/scaled) or 1 (DFT): natural
+  double half;
+  long long n;
+  int lct, plain;
+  __device__ void operator()(long long b, long long j, C v) const {
+    if (plain) {
+      out[b * n + j] = v;
+      return;
+    }
+    double2 o = cmul_d(post[j], to_d2(v));
+    if (lct) {
+      o = cmul_d(rc[b].g, o);
+      if (rc[b].post) {
+        const double x = __dmul_rn((double)(2 * j - n + 1), half);
+        const double y = __dmul_rn(rc[b].s4, x);
+        const double psi = __dmul_rn(rc[b].cout, __dmul_rn(y, y));
+        double s, c;
+        sincos(psi, &s, &c);
+        o = cmul_d(make_double2(c, s), o);
+      }
+    }
+    out[b * n + j] = to_c<C>(o);
+  }
+};
+
+template <class C>
+struct PostChirpZ {
+  C* out;
+  const RowChirp* rc;
+  const double2* post;  // chirp_j / M [* C(n) p_j]
+  double half;
+  long long n;
+  int lct;
+  __device__ void operator()(long long b, long long j, C v) const {
+    if (j >= n) return;
+    double2 o = cmul_d(post[j], to_d2(v));
+    if (lct) {
+      o = cmul_d(rc[b].g, o);
+      if (rc[b].post) {
+        const double x = __dmul_rn((double)(2 * j - n + 1), half);
+        const double y = __dmul_rn(rc[b].s4, x);
+        const double psi = __dmul_rn(rc[b].cout, __dmul_rn(y, y));
+        double s, c;
+        sincos(psi, &s, &c);
+        o = cmul_d(make_double2(c, s), o);
+      }
+    }
+    out[b * n + j] = to_c<C>(o);
+  }
+};
+
+struct PostMehler {
+  double2* out;
+  const OpMehlerRow* rows;
+  const int* rowlist;
+  double half;
+  long long n;
+  __device__ void operator()(long long b, long long m, double2 v) const {
+    const long long row = rowlist[b];
+    const OpMehlerRow p = rows[row];
+    if (m >= p.wn) return;
+    const long long k = p.k0 + m;
+    const double x = (double)(2 * k - n + 1) * half;
+    const double x2 = x * x;
+    out[row * n + k] = cmul_d(cmul_d(p.scale, cexp_d(-p.gam.x * x2, -p.gam.y * x2)), v);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+template <class C, int LOGL, bool LC, bool SC, int SIGN, class Op>
+int launch_tile(long long ntiles, const Op& op, cudaStream_t st) {
+  constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
+  constexpr int W = tile_w<C>();
+  constexpr int E = tile_e<C>(LOGL);
+  constexpr int T = W * ((1 << LOGL) / E);
+  constexpr size_t SM = tile_smem<C, LOGL, W>();
+  auto kern = xft_tile_kernel<C, LOGL, E, W, LC, SC, SIGN, Op>;
+  Tables tb;
+  int rc = get_tables(int64_t(1) << LOGL, dtype, &tb, E);
+  if (rc) return rc;
+  if (SM > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM) != cudaSuccess)
+    return XFT_ECUDA;
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, SM);
+  const long long cap = (long long)sms * (occ < 1 ? 1 : occ);
+  kern<<<(unsigned)(ntiles < cap ? ntiles : cap), T, SM, st>>>(ntiles, op, static_cast<const C*>(tb.tw));
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+constexpr int LMIN = 6, LMAX = 10;  // per-pass lengths 64 .. 1024  =>  M up to 2^20
+
+template <class C, bool LC, bool SC, int SIGN, class Op, int... Ls>
+int tile_dispatch(int l, long long ntiles, const Op& op, cudaStream_t st, std::integer_sequence<int, Ls...>) {
+  int rc = XFT_ENOTSUP;
+  ((l == Ls + LMIN ? (rc = launch_tile<C, Ls + LMIN, LC, SC, SIGN, Op>(ntiles, op, st), 0) : 0), ...);
+  return rc;
+}
+
+template <class C, bool LC, bool SC, int SIGN, class Op>
+int tile(int l, long long ntiles, const Op& op, cudaStream_t st) {
+  if (l < LMIN || l > LMAX) return XFT_ENOTSUP;
+  return tile_dispatch<C, LC, SC, SIGN, Op>(l, ntiles, op, st, std::make_integer_sequence<int, LMAX - LMIN + 1>{});
+}
+
+// samples outside a Mehler row's window: exact zeros
+__global__ void mehler_zero_kernel(double2* out, const int* rowlist, const OpMehlerRow* prm, long long n) {
+  const long long row = rowlist[blockIdx.x];
+  const int k0 = prm[row].k0;
+  for (int k = threadIdx.x; k < k0; k += blockDim.x) {
+    out[row * n + k] = make_double2(0.0, 0.0);
+    out[row * n + n - 1 - k] = make_double2(0.0, 0.0);
+  }
+}
+
+__global__ void row_chirp_kernel(RowChirp* out, long long rows, const double* abcd, long long stride, Abcd uni,
+                                 int bare) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  OpChirpZ op{};
+  op.abcd = abcd;
+  op.abcd_stride = stride;
+  op.uni = uni;
+  op.lct = 1;
+  op.bare = bare;
+  const ChirpZRow c = chirpz_row(op, r);
+  RowChirp o;
+  o.cin = c.cin;
+  o.cout = c.cout;
+  o.s4 = c.s4;
+  o.g = c.g;
+  o.pre = c.pre;
+  o.post = c.post;
+  out[r] = o;
+}
+
+template <class T>
+struct DevBuf {  // stream-ordered scratch
+  T* p = nullptr;
+  cudaStream_t st;
+  explicit DevBuf(cudaStream_t s) : st(s) {}
+  int alloc(size_t count) { return cudaMallocAsync((void**)&p, count * sizeof(T), st) == cudaSuccess ? XFT_OK : XFT_ECUDA; }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+int log2_of(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+// boundary phase p_k and C(n) p_k (natural, fp64) for the large pow2 path
+std::mutex g_pmu;
+std::map<std::pair<int, int64_t>, std::pair<double2*, double2*>> g_ptab;
+int boundary_tables(int64_t n, const double2** p, const double2** cp) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_pmu);
+  auto it = g_ptab.find({dev, n});
+  if (it == g_ptab.end()) {
+    std::vector<double2> a(n), b(n);
+    const int64_t red = (int64_t)(((__int128)(n - 1) * (n - 1)) % (4 * (__int128)n));
+    const std::complex<long double> cn =
+        (PI_L / sqrtl(2.0L * n)) *
+        std::complex<long double>(cosl(PI_L * red / (2.0L * n)), -sinl(PI_L * red / (2.0L * n)));
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t rk = (int64_t)(((__int128)(n - 1) * k) % (2 * (__int128)n));
+      const std::complex<long double> pk(cosl(PI_L * rk / (long double)n), sinl(PI_L * rk / (long double)n));
+      const std::complex<long double> q = pk * cn;
+      a[k] = make_double2((double)pk.real(), (double)pk.imag());
+      b[k] = make_double2((double)q.real(), (double)q.imag());
+    }
+    double2 *da = nullptr, *db = nullptr;
+    if (cudaMalloc(&da, n * 16) != cudaSuccess || cudaMalloc(&db, n * 16) != cudaSuccess) return XFT_ECUDA;
+    if (cudaMemcpy(da, a.data(), n * 16, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(db, b.data(), n * 16, cudaMemcpyHostToDevice) != cudaSuccess)
+      return XFT_ECUDA;
+    it = g_ptab.emplace(std::make_pair(dev, n), std::make_pair(da, db)).first;
+  }
+  *p = it->second.first;
+  *cp = it->second.second;
+  return XFT_OK;
+}
+
+template <class C>
+int large_pow2(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, const double* abcd,
+               int64_t stride, Abcd uni, int flags, cudaStream_t st) {
+  constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
+  constexpr int W = tile_w<C>();
+  const int l = log2_of(n);
+  const Shape sh = split(l);
+  const int M1 = 1 << sh.l1, M2 = 1 << sh.l2;
+  const void* twm = nullptr;
+  int rc = natural_twiddles(sh.M, dtype, &twm);
+  if (rc) return rc;
+  DevBuf<C> scr(st);
+  DevBuf<RowChirp> rcs(st);
+  if ((rc = scr.alloc((size_t)batch * sh.M))) return rc;
+  const double2 *ptab = nullptr, *cptab = nullptr;
+  if (mode != MODE_DFT && (rc = boundary_tables(n, &ptab, &cptab))) return rc;
+  if (mode == MODE_LCT) {
+    if ((rc = rcs.alloc(batch))) return rc;
+    row_chirp_kernel<<<(unsigned)((batch + 127) / 128), 128, 0, st>>>(rcs.p, batch, abcd, stride, uni,
+                                                                      (flags & XFT_FLAG_BARE_FOURIER) ? 1 : 0);
+  }
+  const long long t1 = batch * (M2 / W), t2 = batch * (M1 / W);
+  PostLct<C> post{static_cast<C*>(out), rcs.p, cptab, host_half_step(n), n, mode == MODE_LCT, mode == MODE_DFT};
+  if (mode == MODE_DFT) {
+    OpCols<C, GenLoad<C>> op1{GenLoad<C>{static_cast<const C*>(in), nullptr, sh.M}, scr.p,
+                              static_cast<const C*>(twm), M2, W, sh.M, sign > 0};
+    OpRowsNat<C, PostLct<C>> op2{scr.p, post, M1, M2, W, sh.M};
+    if (sign < 0) {
+      if ((rc = tile<C, true, true, -1>(sh.l1, t1, op1, st))) return rc;
+      return tile<C, false, true, -1>(sh.l2, t2, op2, st);
+    }
+    if ((rc = tile<C, true, true, +1>(sh.l1, t1, op1, st))) return rc;
+    return tile<C, false, true, +1>(sh.l2, t2, op2, st);
+  }
+  OpCols<C, GenLct<C>> op1{GenLct<C>{static_cast<const C*>(in), rcs.p, ptab, host_half_step(n), n, mode == MODE_LCT},
+                           scr.p, static_cast<const C*>(twm), M2, W, sh.M, 0};
+  OpRowsNat<C, PostLct<C>> op2{scr.p, post, M1, M2, W, sh.M};
+  if ((rc = tile<C, true, true, -1>(sh.l1, t1, op1, st))) return rc;
+  return tile<C, false, true, -1>(sh.l2, t2, op2, st);
+}
+
+}  // namespace
+
+namespace xftb {
+
+// rows longer than the in-CTA kernels: four-step path (power-of-two n)
+int run_large_pow2(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype,
+                   const double* abcd, int64_t stride, const double* uni4, int flags, cudaStream_t st) {
+  const int l = log2_of(n);
+  if ((int64_t(1) << l) != n || l > 2 * LMAX || (l + 1) / 2 < LMIN) return XFT_ENOTSUP;
+  const Abcd uni = uni4 ? Abcd{uni4[0], uni4[1], uni4[2], uni4[3]} : Abcd{0, 0, 0, 0};
+  return dtype == XFT_C64 ? large_pow2<float2>(mode, sign, in, out, batch, n, abcd, stride, uni, flags, st)
+                          : large_pow2<double2>(mode, sign, in, out, batch, n, abcd, stride, uni, flags, st);
+}
+
+// Mehler rows whose window needs M > in-CTA limit (complex128)
+int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm,
+                     int l, int64_t n, cudaStream_t st) {
+  using C = double2;
+  constexpr int W = tile_w<C>();
+  const Shape sh = split(l);
+  const int M1 = 1 << sh.l1, M2 = 1 << sh.l2;
+  const void* twm = nullptr;
+  int rc = natural_twiddles(sh.M, XFT_C128, &twm);
+  if (rc) return rc;
+  DevBuf<C> hs(st), us(st);
+  if ((rc = hs.alloc((size_t)rows * sh.M)) || (rc = us.alloc((size_t)rows * sh.M))) return rc;
+  const long long t1 = rows * (M2 / W), t2 = rows * (M1 / W);
+  const double half = host_half_step(n);
+  // kernel spectrum, permuted
+  OpCols<C, GenMehlerH> h1{GenMehlerH{prm, rowlist, sh.M}, hs.p, static_cast<const C*>(twm), M2, W, sh.M, 0};
+  if ((rc = tile<C, true, true, -1>(sh.l1, t1, h1, st))) return rc;
+  OpRowsPerm<C> h2{hs.p, M1, M2, W, sh.M};
+  if ((rc = tile<C, false, false, -1>(sh.l2, t2, h2, st))) return rc;
+  // data: columns, rows (forward x H inverse), inverse columns with the output weights
+  OpCols<C, GenMehlerU> u1{GenMehlerU{static_cast<const C*>(in), prm, rowlist, half, n}, us.p,
+                           static_cast<const C*>(twm), M2, W, sh.M, 0};
+  if ((rc = tile<C, true, true, -1>(sh.l1, t1, u1, st))) return rc;
+  OpRowsConv<C> u2{us.p, hs.p, sh.M, static_cast<const C*>(twm), M1, M2, W, sh.M};
+  if ((rc = tile<C, false, false, -1>(sh.l2, t2, u2, st))) return rc;
+  OpColsInv<C, PostMehler> u3{us.p, PostMehler{static_cast<C*>(out), prm, rowlist, half, n}, M2, W, sh.M};
+  if ((rc = tile<C, true, true, +1>(sh.l1, t1, u3, st))) return rc;
+  mehler_zero_kernel<<<(unsigned)rows, 256, 0, st>>>(static_cast<C*>(out), rowlist, prm, n);
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+}  // namespace xftb

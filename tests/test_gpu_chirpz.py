@@ -142,3 +142,38 @@ def test_mehler_hermite_eigen(torch, X):
     for m in range(8):
         ref = math.sqrt(2 * math.pi) * z ** m * psi[m]
         assert rel_l2(got[m], ref) <= 1e-10, m
+
+
+def test_mehler_config3_full(torch, X):
+    """Config 3 at full size (1024 x 16384, c128): every size class, incl. the four-step rows.
+
+    Sampled rows/outputs against the chunked dense oracle, and every row against the
+    Hermite-Gaussian eigen-relation K_z psi_m ~ sqrt(2 pi) z^m psi_m (inputs are psi_m + 1e-6 noise).
+    """
+    from paper_0912_1379_b200 import workloads
+
+    c3 = workloads.config3()
+    z = c3.extra["z"]
+    got_t = X.mehler_rows(dev(torch, c3.values), z)
+    got = got_t.cpu().numpy()
+    n = 16384
+    # window class of each row (same rule as the library): widest windows exercise the four-step path
+    gam = np.where((2 * z / (1 - z * z)).real >= 0, (1 - z) / (2 * (1 + z)), (1 + z) / (2 * (1 - z))).real
+    rows = list(np.argsort(gam)[:4]) + list(np.argsort(gam)[-2:]) + [0, 1, 511]
+    js = np.linspace(0, n - 1, 97).astype(int)
+    js = np.unique(np.concatenate([js, n // 2 + np.arange(-40, 40, 7)]))
+    for r in rows:
+        ref = O.mehler_apply(z[r], c3.values[r], rows_out=js)
+        assert rel_l2(got[r, js], ref) <= _mehler_tol(z[r]), (r, z[r])
+    # every row: linearity M(psi + noise) = M(psi) + M(noise), and the Hermite-Gaussian
+    # eigen-relation M(psi_m) ~ sqrt(2 pi) z^m psi_m (continuum limit)
+    x = X.asymptotic_zeros(n).nodes
+    psi = X.hermite_function_table(31, x)[c3.extra["m"]].astype(complex)
+    g_psi = X.mehler_rows(dev(torch, psi), z)
+    g_noise = X.mehler_rows(dev(torch, c3.values - psi), z)
+    lin = ((got_t - g_psi - g_noise).abs() ** 2).sum(1).sqrt() / (got_t.abs() ** 2).sum(1).sqrt()
+    assert float(lin.max()) <= 1e-12
+    g_psi = g_psi.cpu().numpy()
+    for r in range(z.shape[0]):
+        ideal = math.sqrt(2 * math.pi) * z[r] ** c3.extra["m"][r] * psi[r]
+        assert np.linalg.norm(g_psi[r] - ideal) <= 1e-6 * max(np.linalg.norm(ideal), 1e-9), r

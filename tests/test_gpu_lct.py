@@ -71,7 +71,7 @@ def test_lct_golden_c64(torch, X, golden, n):
     assert max_row_rel_l2(got, ref) <= TOL64
 
 
-POW2 = [1, 2, 4, 8, 16, 32, 64, 128, 512, 1024, 2048, 4096, 8192, 16384]
+POW2 = [1, 2, 4, 8, 16, 32, 64, 128, 512, 1024, 2048, 4096, 8192, 16384, 32768]
 
 
 @pytest.mark.parametrize("n", POW2)
