@@ -114,12 +114,26 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
 /* Host check of z values (FrftOrder / mehler_kernel, xft/dense.py:49-59, 127-130). */
 int xft_validate_mehler_z(const double* z, int64_t count, int64_t stride, int64_t* bad_row);
 
-/* Separable 2-D LCT on one device: fast LCT along rows (abcd_row) then along
- * columns (abcd_col) of an n_rows x n_cols field.  `workspace`: device scratch
- * of n_rows*n_cols complex elements (dtype).  Composition of fast_lct along
- * axis 1 then axis 0 (no reference symbol; SURVEY 8(a) last row). */
+/* Separable 2-D LCT on one device: fast LCT along rows (abcd_row, host) then
+ * along columns (abcd_col, host) of an n_rows x n_cols field (device in/out).
+ * `workspace`: device scratch of n_rows*n_cols complex elements (dtype).
+ * Composition of fast_lct along axis 1 then axis 0 (no reference symbol;
+ * SURVEY 8(a) last row). */
 int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dtype, const double* abcd_row,
               const double* abcd_col, void* workspace, void* stream);
+
+/* Column LCT of a [n_rows][n_cols] slab with row stride ld (device in/out,
+ * abcd on the host): the second axis of the separable 2-D LCT and the receive
+ * side of the sharded 2-D transform.  In place allowed.  `workspace`: n_rows*ld
+ * elements (used when n_rows > 1024).  n_rows: power of two >= 64. */
+int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, int64_t ld, int dtype,
+                    const double* abcd_host, void* workspace, void* stream);
+
+/* Row LCT (one quadruple, host) written in the all-to-all send layout of the
+ * sharded 2-D transform: segment g (2^seg_log2w samples) of row r is stored at
+ * out + g*seg_stride + r*2^seg_log2w.  seg_stride >= batch * 2^seg_log2w. */
+int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd_host,
+                        int seg_log2w, int64_t seg_stride, void* stream);
 
 /* Tiled transpose used by the 2-D pass and the sharded all-to-all layout:
  * out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols. */

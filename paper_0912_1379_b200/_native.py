@@ -47,6 +47,8 @@ _SIGS = {
     "xft_validate_mehler_z": ([_vp, _i64, _i64, ctypes.POINTER(_i64)], ctypes.c_int),
     "xft_lct2d": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp], ctypes.c_int),
     "xft_transpose": ([_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
+    "xft_lct_columns": ([_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
+    "xft_lct_rows_packed": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, ctypes.c_int, _i64, _vp], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

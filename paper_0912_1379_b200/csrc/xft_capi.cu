@@ -27,6 +27,8 @@ struct LaunchArgs {
   Tables tb;
   int flags;
   cudaStream_t st;
+  int seg_log2w = 0;        // segmented (all-to-all send) output layout
+  long long seg_stride = 0;  // 0: natural rows
 };
 
 using LaunchFn = int (*)(const LaunchArgs&);
@@ -123,7 +125,8 @@ int launch_pipe(const LaunchArgs& a) {
   }
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
       static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, coefs, per_row,
-      static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc);
+      static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc, a.seg_log2w,
+      a.seg_stride);
   if (coefs) cudaFreeAsync(coefs, a.st);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
 }
@@ -155,7 +158,8 @@ int log2_exact(int64_t n) {
 }
 
 int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype,
-             const double* abcd, int64_t stride, Abcd uni, int flags, cudaStream_t st) {
+             const double* abcd, int64_t stride, Abcd uni, int flags, cudaStream_t st, int seg_log2w = 0,
+             long long seg_stride = 0) {
   if (n < 1) return XFT_EINVALID_SIZE;
   if (batch < 0) return XFT_EINVALID_SIZE;
   if (dtype != XFT_C64 && dtype != XFT_C128) return XFT_EPARAM;
@@ -170,6 +174,9 @@ int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64
     return run_large_pow2(mode, sign, in, out, batch, n, dtype, abcd, stride, u4, flags, st);
   }
   LaunchArgs a{in, out, (long long)batch, abcd, (long long)stride, uni, {}, flags, st};
+  a.seg_log2w = seg_log2w;
+  a.seg_stride = seg_stride;
+  if (seg_stride && (seg_log2w > l || mode != MODE_LCT)) return XFT_EPARAM;
   int rc = get_tables(n, dtype, &a.tb);
   if (rc) return rc;
   LaunchFn fn = nullptr;
@@ -294,10 +301,13 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
   auto st = static_cast<cudaStream_t>(stream);
   const Abcd ur{abcd_row[0], abcd_row[1], abcd_row[2], abcd_row[3]};
   const Abcd uc{abcd_col[0], abcd_col[1], abcd_col[2], abcd_col[3]};
-  // rows -> out ; transpose out -> ws ; rows of ws (= columns) -> out ; transpose out -> ws ; copy-free:
-  // the final transpose writes the caller's buffer.
+  // axis 1: rows (in -> out); axis 0: columns in place on `out` (workspace = four-step scratch)
   rc = run_rows(MODE_LCT, -1, in, out, n_rows, n_cols, dtype, nullptr, 0, ur, 0, st);
-  if (!rc) rc = xft_transpose(out, workspace, n_rows, n_cols, n_cols, n_rows, dtype, stream);
+  if (rc) return rc;
+  rc = run_lct_cols(out, out, workspace, n_rows, n_cols, n_cols, dtype, abcd_col, 0, st);
+  if (rc != XFT_ENOTSUP) return rc;
+  // other shapes: transpose, transform the (former) columns as rows, transpose back
+  rc = xft_transpose(out, workspace, n_rows, n_cols, n_cols, n_rows, dtype, stream);
   if (!rc) rc = run_rows(MODE_LCT, -1, workspace, out, n_cols, n_rows, dtype, nullptr, 0, uc, 0, st);
   if (!rc) rc = xft_transpose(out, workspace, n_cols, n_rows, n_rows, n_cols, dtype, stream);
   if (!rc) {
@@ -306,6 +316,24 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
       rc = XFT_ECUDA;
   }
   return rc;
+}
+
+int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, int64_t ld, int dtype,
+                    const double* abcd_host, void* workspace, void* stream) {
+  if (n_rows < 1 || n_cols < 1 || ld < n_cols) return XFT_EINVALID_SIZE;
+  int rc = xft_validate_lct_params(abcd_host, 1, 0, 1, 1e-10, nullptr);
+  if (rc) return rc;
+  return run_lct_cols(in, out, workspace, n_rows, n_cols, ld, dtype, abcd_host, 0, static_cast<cudaStream_t>(stream));
+}
+
+int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd_host,
+                        int seg_log2w, int64_t seg_stride, void* stream) {
+  int rc = xft_validate_lct_params(abcd_host, 1, 0, 1, 1e-10, nullptr);
+  if (rc) return rc;
+  if (seg_stride < (int64_t)batch << seg_log2w) return XFT_ESHAPE;
+  const Abcd u{abcd_host[0], abcd_host[1], abcd_host[2], abcd_host[3]};
+  return run_rows(MODE_LCT, -1, in, out, batch, n, dtype, nullptr, 0, u, 0, static_cast<cudaStream_t>(stream),
+                  seg_log2w, seg_stride);
 }
 
 int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,

@@ -22,4 +22,9 @@ struct OpMehlerRow;
 int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm, int l,
                      int64_t n, cudaStream_t st);
 
+// column LCT of a [R][ncols] slab with row stride ld (xft_large.cu); abcd on the host.
+// ws: scratch of R*ld elements when R > 1024.
+int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, int dtype,
+                 const double* abcd_host, int flags, cudaStream_t st);
+
 }  // namespace xftb

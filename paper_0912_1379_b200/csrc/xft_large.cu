@@ -570,3 +570,222 @@ int run_large_mehler(const void* in, void* out, long long rows, const int* rowli
 }
 
 }  // namespace xftb
+
+// ---------------------------------------------------------------------------
+// column LCT of a [R][ncols] slab (row stride ld), one parameter quadruple:
+// the second axis of the separable 2-D transform.  Lines are columns, so every
+// access moves W adjacent columns; R <= 1024 in one pass, larger R by the
+// four-step split R = R1 R2 (pass 1 over r1 with the twiddle, pass 2 over r2
+// storing straight to the natural row index j = k1 + R1 k2).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct ColChirp {               // host-computed, uniform over the slab
+  // c64: exact fixed-point turns (see xft_pipe.cuh)
+  unsigned long long dq_in, dq_out;
+  unsigned gq;
+  float gabs;
+  // c128: exact fp64 phase arguments
+  double cin, cout, s4, half;
+  double2 g;
+  int pre, post, log2r;
+  long long R;
+};
+
+template <class C>
+struct ColPhase;
+
+template <>
+struct ColPhase<float2> {
+  static __device__ __forceinline__ float2 pre(const ColChirp& k, const double2*, long long r, float2 v) {
+    const int off = (int)(2 * r - k.R + 1);
+    const unsigned o2 = (unsigned)(off * off);
+    const unsigned bt = ((unsigned)(r & 1) << 31) - ((unsigned)r << (31 - k.log2r));
+    unsigned top = bt;
+    if (k.pre) top += (unsigned)(k.dq_in >> 32) * o2 + __umulhi((unsigned)k.dq_in, o2);
+    return cmul(unit_turns_sfu(top, 1.0f), v);
+  }
+  static __device__ __forceinline__ float2 post(const ColChirp& k, const double2*, long long j, float2 v) {
+    const int off = (int)(2 * j - k.R + 1);
+    const unsigned o2 = (unsigned)(off * off);
+    const unsigned bt = ((unsigned)(j & 1) << 31) - ((unsigned)j << (31 - k.log2r));
+    unsigned top = bt + k.gq;
+    if (k.post) top += (unsigned)(k.dq_out >> 32) * o2 + __umulhi((unsigned)k.dq_out, o2);
+    return cmul(unit_turns_sfu(top, k.gabs), v);
+  }
+};
+
+template <>
+struct ColPhase<double2> {
+  static __device__ __forceinline__ double2 pre(const ColChirp& k, const double2* ptab, long long r, double2 v) {
+    double2 u = cmul_d(ptab[r], v);
+    if (k.pre) {
+      const double x = __dmul_rn((double)(2 * r - k.R + 1), k.half);
+      const double phi = __dmul_rn(k.cin, __dmul_rn(x, x));
+      double s, c;
+      sincos(phi, &s, &c);
+      u = cmul_d(make_double2(c, s), u);
+    }
+    return u;
+  }
+  static __device__ __forceinline__ double2 post(const ColChirp& k, const double2* cptab, long long j, double2 v) {
+    double2 o = cmul_d(cmul_d(k.g, cptab[j]), v);
+    if (k.post) {
+      const double x = __dmul_rn((double)(2 * j - k.R + 1), k.half);
+      const double y = __dmul_rn(k.s4, x);
+      const double psi = __dmul_rn(k.cout, __dmul_rn(y, y));
+      double s, c;
+      sincos(psi, &s, &c);
+      o = cmul_d(make_double2(c, s), o);
+    }
+    return o;
+  }
+};
+
+template <class C>
+struct OpColLctOne {  // R <= 1024
+  static constexpr bool MID = false;
+  const C* in;
+  C* out;
+  long long ld;
+  int W;
+  ColChirp k;
+  const double2 *ptab, *cptab;
+  __device__ C load(long long tile, int w, int a) const {
+    const long long c = tile * W + w;
+    return ColPhase<C>::pre(k, ptab, a, in[(long long)a * ld + c]);
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    const long long c = tile * W + w;
+    out[(long long)a * ld + c] = ColPhase<C>::post(k, cptab, a, v);
+  }
+};
+
+template <class C>
+struct OpColLct1 {  // four-step pass 1: DFT over r1 for the line (r2, c); twiddle w_R^{k1 r2}
+  static constexpr bool MID = false;
+  const C* in;
+  C* scr;
+  long long ld;
+  int W, ncols, R2;
+  ColChirp k;
+  const double2* ptab;
+  const C* twr;  // natural twiddles of length R
+  __device__ C load(long long tile, int w, int a) const {
+    const int cb = ncols / W;
+    const long long r2 = tile / cb, c = (tile % cb) * W + w;
+    const long long r = (long long)a * R2 + r2;
+    return ColPhase<C>::pre(k, ptab, r, in[r * ld + c]);
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    const int cb = ncols / W;
+    const long long r2 = tile / cb, c = (tile % cb) * W + w;
+    scr[((long long)a * R2 + r2) * ld + c] = cmul(v, twr[(long long)a * r2]);
+  }
+};
+
+template <class C>
+struct OpColLct2 {  // pass 2: DFT over r2 for the line (k1, c); natural row j = k1 + R1 k2
+  static constexpr bool MID = false;
+  const C* scr;
+  C* out;
+  long long ld;
+  int W, ncols, R1, R2;
+  ColChirp k;
+  const double2* cptab;
+  __device__ C load(long long tile, int w, int a) const {
+    const int cb = ncols / W;
+    const long long k1 = tile / cb, c = (tile % cb) * W + w;
+    return scr[(k1 * R2 + a) * ld + c];
+  }
+  __device__ void store(long long tile, int w, int a, C v) const {
+    const int cb = ncols / W;
+    const long long k1 = tile / cb, c = (tile % cb) * W + w;
+    const long long j = k1 + (long long)R1 * a;
+    out[j * ld + c] = ColPhase<C>::post(k, cptab, j, v);
+  }
+};
+
+unsigned long long frac_q64_host(long double v) {
+  long double f = v - floorl(v);
+  if (!(f >= 0.0L && f < 1.0L)) f = 0.0L;
+  return (unsigned long long)(f * 18446744073709551616.0L);
+}
+
+ColChirp col_chirp(const double* abcd, int64_t R, int bare) {
+  ColChirp k{};
+  const double a = abcd[0], b = abcd[1], d = abcd[3];
+  k.cin = (0.5 * a) / b;  // IEEE double division: the reference's (0.5j * a / b).imag
+  k.cout = (0.5 * d) / b;
+  k.s4 = (4.0 * b) / 3.141592653589793116;
+  k.half = host_half_step(R);
+  k.pre = a != 0.0;
+  k.post = d != 0.0;
+  k.R = R;
+  int l = 0;
+  while ((int64_t(1) << l) < R) ++l;
+  k.log2r = l;
+  const long double h2 = (long double)k.half * k.half;
+  const long double i2pi = 1.0L / (2.0L * PI_L);
+  k.dq_in = frac_q64_host(k.cin * h2 * i2pi);
+  k.dq_out = frac_q64_host(k.cout * (long double)k.s4 * k.s4 * h2 * i2pi);
+  const int64_t red = (int64_t)(((__int128)(R - 1) * (R - 1)) % (4 * (__int128)R));
+  unsigned long long gq = 0ull - ((unsigned long long)red << (62 - l));
+  gq += (b > 0.0) ? (0ull - (1ull << 61)) : (1ull << 61);
+  if (bare) gq += (1ull << 61);
+  k.gq = (unsigned)(gq >> 32);
+  const long double gabs = (PI_L / sqrtl(2.0L * R)) / sqrtl(2.0L * PI_L * fabsl((long double)b)) * (bare ? sqrtl(2.0L * PI_L) : 1.0L);
+  k.gabs = (float)gabs;
+  // c128 row factor e^{-i pi sgn(b)/4}/sqrt(2 pi |b|) [* sqrt(2 pi i)] (C(n) p_j is in cptab)
+  const long double h = 0.70710678118654752440L / sqrtl(2.0L * PI_L * fabsl((long double)b));
+  long double gx = h, gy = b > 0.0 ? -h : h;
+  if (bare) {
+    const long double sp = sqrtl(PI_L);
+    const long double ux = (gx - gy) * sp, uy = (gx + gy) * sp;
+    gx = ux;
+    gy = uy;
+  }
+  k.g = make_double2((double)gx, (double)gy);
+  return k;
+}
+
+template <class C>
+int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, const double* abcd, int bare,
+             cudaStream_t st) {
+  constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
+  constexpr int W = tile_w<C>();
+  if (ncols % W) return XFT_ENOTSUP;
+  const int l = log2_of(R);
+  const ColChirp k = col_chirp(abcd, R, bare);
+  const double2 *ptab = nullptr, *cptab = nullptr;
+  int rc = boundary_tables(R, &ptab, &cptab);
+  if (rc) return rc;
+  if (l <= LMAX) {
+    OpColLctOne<C> op{static_cast<const C*>(in), static_cast<C*>(out), ld, W, k, ptab, cptab};
+    return tile<C, true, true, -1>(l, ncols / W, op, st);
+  }
+  const Shape sh = split(l);
+  const int R1 = 1 << sh.l1, R2 = 1 << sh.l2;
+  const void* twr = nullptr;
+  if ((rc = natural_twiddles(R, dtype, &twr))) return rc;
+  OpColLct1<C> op1{static_cast<const C*>(in), static_cast<C*>(ws), ld, W, (int)ncols, R2, k, ptab,
+                   static_cast<const C*>(twr)};
+  if ((rc = tile<C, true, true, -1>(sh.l1, (long long)R2 * (ncols / W), op1, st))) return rc;
+  OpColLct2<C> op2{static_cast<const C*>(ws), static_cast<C*>(out), ld, W, (int)ncols, R1, R2, k, cptab};
+  return tile<C, true, true, -1>(sh.l2, (long long)R1 * (ncols / W), op2, st);
+}
+
+}  // namespace
+
+namespace xftb {
+
+int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, int dtype,
+                 const double* abcd_host, int flags, cudaStream_t st) {
+  const int l = log2_of(R);
+  if ((int64_t(1) << l) != R || l < LMIN || l > 2 * LMAX) return XFT_ENOTSUP;
+  const int bare = (flags & XFT_FLAG_BARE_FOURIER) ? 1 : 0;
+  return dtype == XFT_C64 ? lct_cols<float2>(in, out, ws, R, ncols, ld, abcd_host, bare, st)
+                          : lct_cols<double2>(in, out, ws, R, ncols, ld, abcd_host, bare, st);
+}
+
+}  // namespace xftb

@@ -397,8 +397,22 @@ __device__ __forceinline__ void pre_multiply(typename Cfg::C (&v)[Cfg::E], const
   }
 }
 
+// output addressing of one row: natural (seg_stride == 0) or split into
+// 2^segl-wide segments placed seg_stride apart (the all-to-all send layout of
+// the sharded 2-D transform: segment g of row r lands at g*seg_stride + r*2^segl)
+template <class C>
+struct OutRow {
+  C* base;  // natural: row start; segmented: out + r * 2^segl
+  long long seg_stride;
+  int segl;
+  __device__ __forceinline__ C* at(int c) const {
+    if (seg_stride == 0) return base + c;
+    return base + (long long)(c >> segl) * seg_stride + (c & ((1 << segl) - 1));
+  }
+};
+
 template <class Cfg>
-__device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* __restrict__ dst, int j,
+__device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const OutRow<typename Cfg::C>& dst, int j,
                                            const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
                                            const RowConst& kc, double2 cn, const typename Cfg::C* __restrict__ ptab,
                                            const void* tabv) {
@@ -406,16 +420,16 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], typenam
   constexpr int E = Cfg::E, TR = Cfg::TR;
   if constexpr (Cfg::MODE == MODE_DFT) {
 #pragma unroll
-    for (int s = 0; s < E; ++s) st_stream(dst + j + s * TR, v[s]);
+    for (int s = 0; s < E; ++s) st_stream(dst.at(j + s * TR), v[s]);
   } else if constexpr (Cfg::MODE == MODE_SCALED) {
     const C c = to_c<C>(cn);
 #pragma unroll
-    for (int s = 0; s < E; ++s) st_stream(dst + j + s * TR, cmul(c, cmul(__ldg(&ptab[j + s * TR]), v[s])));
+    for (int s = 0; s < E; ++s) st_stream(dst.at(j + s * TR), cmul(c, cmul(__ldg(&ptab[j + s * TR]), v[s])));
   } else {
     if (rcs.post == 0) {
       const C g = rcs.g;
 #pragma unroll
-      for (int s = 0; s < E; ++s) st_stream(dst + j + s * TR, cmul(cmul(g, __ldg(&ptab[j + s * TR])), v[s]));
+      for (int s = 0; s < E; ++s) st_stream(dst.at(j + s * TR), cmul(cmul(g, __ldg(&ptab[j + s * TR])), v[s]));
       return;
     }
     if constexpr (!Cfg::C128) {
@@ -428,7 +442,7 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], typenam
         const int off = tc.off0 + 2 * s * TR;
         const uint32_t o2 = (uint32_t)(off * off);
         const uint32_t top = dhi * o2 + __umulhi(dlo, o2) + (b0 - (uint32_t)s * (1u << (31 - Cfg::LE)));
-        st_stream(dst + j + s * TR, cmul(unit_turns_sfu(top, g), v[s]));
+        st_stream(dst.at(j + s * TR), cmul(unit_turns_sfu(top, g), v[s]));
       }
     } else {
       const double2* tab = static_cast<const double2*>(tabv);
@@ -443,7 +457,7 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], typenam
           const double psi = __dmul_rn(cout, __dmul_rn(y, y));  // xft/kernel.py:113
           const double add = d0 - kStepPi16[s * (16 / E)];
           const double2 e = unit_phase_tab(psi, add, q0, tab);
-          st_stream(dst + j + s * TR, cmul(make_double2(e.x * g, e.y * g), v[s]));
+          st_stream(dst.at(j + s * TR), cmul(make_double2(e.x * g, e.y * g), v[s]));
         }
       } else {
 #pragma unroll
@@ -453,7 +467,7 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], typenam
           const double psi = __dmul_rn(cout, __dmul_rn(y, y));
           const double add = d0 - kStepPi16[s * (16 / E)];
           const double2 e = unit_phase_tab(prereduce(psi), add, q0, tab);
-          st_stream(dst + j + s * TR, cmul(make_double2(e.x * g, e.y * g), v[s]));
+          st_stream(dst.at(j + s * TR), cmul(make_double2(e.x * g, e.y * g), v[s]));
         }
       }
     }
@@ -478,7 +492,8 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restrict__ out, long long batch,
                 const typename Cfg::Coef* __restrict__ coefs, int coef_per_row, const typename Cfg::C* __restrict__ tw,
-                const typename Cfg::C* __restrict__ ptab, const void* __restrict__ gtab, double2 cn, RowConst kc) {
+                const typename Cfg::C* __restrict__ ptab, const void* __restrict__ gtab, double2 cn, RowConst kc,
+                int seg_log2w, long long seg_stride) {
   using C = typename Cfg::C;
   using Coef = typename Cfg::Coef;
   constexpr int N = Cfg::N, ROWS = Cfg::ROWS, S = Cfg::STAGES;
@@ -565,7 +580,10 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
 #pragma unroll
         for (int s = 0; s < Cfg::E; ++s) st_stream(out + row * N + j + s * Cfg::TR, v[s]);
     } else {
-      if (row < batch) post_store<Cfg>(v, out + row * N, j, rc, tc, kc, cn, ptab, tab);
+      if (row < batch) {
+        const OutRow<C> o{seg_stride ? out + (row << seg_log2w) : out + row * N, seg_stride, seg_log2w};
+        post_store<Cfg>(v, o, j, rc, tc, kc, cn, ptab, tab);
+      }
     }
   }
 }

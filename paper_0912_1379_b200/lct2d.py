@@ -2,7 +2,16 @@
 
 No reference symbol exists; the transform is defined as the composition of
 the reference 1-D ``fast_lct`` (xft/lct.py:168-208) along both axes
-(last row).  Single-GPU: ``xft_lct2d`` in libxft_b200.so.
+(last row).
+
+* ``lct2d`` -- one GPU: row kernel, then the column kernels (``xft_lct2d``).
+* ``lct2d_sharded`` -- G ranks (one process per GPU, torch.distributed/NCCL):
+  rank g holds rows [g n/G, (g+1) n/G).  The row kernel writes its output
+  directly in the all-to-all send layout (segment h of every row goes to the
+  block for rank h), one ``all_to_all_single`` over NVLink delivers to every
+  rank the full height of its n/G columns as a row-major [n, n/G] slab, and the
+  column kernels transform that slab in place.  The result stays column-sharded:
+  rank g returns columns [g n/G, (g+1) n/G) of the 2-D transform.
 """
 from __future__ import annotations
 
@@ -10,6 +19,11 @@ import numpy as np
 
 from . import _native, ops
 from .errors import ShapeError
+
+
+def _abcd4(p):
+    a = np.ascontiguousarray(np.asarray(p, dtype=np.float64).reshape(4))
+    return a
 
 
 def lct2d(field, abcd_row, abcd_col=None, *, out=None, workspace=None):
@@ -21,8 +35,7 @@ def lct2d(field, abcd_row, abcd_col=None, *, out=None, workspace=None):
         raise ShapeError("lct2d needs a 2-D CUDA tensor")
     f = field.contiguous()
     r, c = f.shape
-    pr = np.ascontiguousarray(np.asarray(abcd_row, dtype=np.float64).reshape(4))
-    pc = np.ascontiguousarray(np.asarray(abcd_col, dtype=np.float64).reshape(4))
+    pr, pc = _abcd4(abcd_row), _abcd4(abcd_col)
     if out is None:
         out = torch.empty_like(f)
     if workspace is None:
@@ -31,3 +44,60 @@ def lct2d(field, abcd_row, abcd_col=None, *, out=None, workspace=None):
         _native.call("xft_lct2d", f.data_ptr(), out.data_ptr(), r, c, ops._dtype_code(f),
                      pr.ctypes.data, pc.ctypes.data, workspace.data_ptr(), ops._stream_ptr(f.device))
     return out
+
+
+# ---- device building blocks of the sharded transform ------------------------
+def rows_packed(local, abcd_row, world: int, out=None):
+    """Row LCT of the local [rl, n] rows written as the all-to-all send buffer [world, rl, n/world]."""
+    torch = ops._torch()
+    rl, n = local.shape
+    nc = n // world
+    if nc * world != n or nc & (nc - 1):
+        raise ShapeError(f"n = {n} must split into {world} power-of-two column blocks")
+    if out is None:
+        out = torch.empty((world, rl, nc), dtype=local.dtype, device=local.device)
+    p = _abcd4(abcd_row)
+    with torch.cuda.device(local.device):
+        _native.call("xft_lct_rows_packed", local.data_ptr(), out.data_ptr(), rl, n, ops._dtype_code(local),
+                     p.ctypes.data, int(nc).bit_length() - 1, rl * nc, ops._stream_ptr(local.device))
+    return out
+
+
+def columns_inplace(slab, abcd_col, workspace=None):
+    """Column LCT of a row-major [n, nc] slab, in place."""
+    torch = ops._torch()
+    n, nc = slab.shape
+    p = _abcd4(abcd_col)
+    if workspace is None and n > 1024:
+        workspace = torch.empty_like(slab)
+    with torch.cuda.device(slab.device):
+        _native.call("xft_lct_columns", slab.data_ptr(), slab.data_ptr(), n, nc, nc, ops._dtype_code(slab),
+                     p.ctypes.data, 0 if workspace is None else workspace.data_ptr(), ops._stream_ptr(slab.device))
+    return slab
+
+
+def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, col_fn=None, buffers=None):
+    """Sharded 2-D LCT over the ranks of ``group``.
+
+    ``local``: this rank's [n/G, n] rows.  Returns this rank's [n, n/G] column
+    slab of the result.  ``row_fn(local, abcd, world) -> send[world, rl, nc]``
+    and ``col_fn(slab, abcd) -> slab`` default to the CUDA kernels; tests on
+    CPU (gloo) substitute the CPU oracle to check the orchestration/layout.
+    ``buffers``: optional preallocated (send, recv) of shape [world, rl, nc].
+    """
+    import torch
+    import torch.distributed as dist
+
+    if abcd_col is None:
+        abcd_col = abcd_row
+    world = dist.get_world_size(group)
+    rl, n = local.shape
+    if rl * world != n:
+        raise ShapeError(f"{world} ranks x {rl} rows do not tile an n = {n} field")
+    nc = n // world
+    row_fn = row_fn or (lambda x, p, w: rows_packed(x, p, w, out=None if buffers is None else buffers[0]))
+    col_fn = col_fn or columns_inplace
+    send = row_fn(local, abcd_row, world)
+    recv = torch.empty_like(send) if buffers is None else buffers[1]
+    dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+    return col_fn(recv.view(n, nc), abcd_col)
