@@ -109,46 +109,77 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# workloads
+# workloads: each item is one transform launched once per step
 # ---------------------------------------------------------------------------
-def make_workload(name: str, rows_override=None):
+class Item:
+    """tag, host input, parameters, kind in {lct, mehler, lct2d}; alg_bytes = HBM bytes the op must move."""
+
+    def __init__(self, tag, kind, values, params, samples=None, alg_bytes=None, extra=None):
+        self.tag, self.kind, self.values, self.params = tag, kind, values, params
+        self.samples = values.size if samples is None else samples
+        self.alg_bytes = values.nbytes * 2 if alg_bytes is None else alg_bytes
+        self.extra = extra or {}
+
+
+def make_workload(name: str, rows_override=None, rank=0, world=1):
     from paper_0912_1379_b200 import workloads as W
 
     if name == "cfg2":
         rows = rows_override or 4096
         c64 = W.config2(rows=rows, n=4096, dtype=np.complex64)
         c128 = W.config2(rows=rows, n=4096, dtype=np.complex128)
-        return [("c64", c64.values, c64.abcd), ("c128", c128.values, c128.abcd)], \
+        return [Item("c64", "lct", c64.values, c64.abcd), Item("c128", "lct", c128.values, c128.abcd)], \
             {"workload": f"cfg2 batched FrFT {rows}x4096 c64+c128, per-row alpha~U(0,pi) seed 1",
              "rows": rows, "n": 4096}
     if name == "cfg4":
         c4 = W.config4(rows=rows_override or 65536)
-        return [("c64", c4.values, c4.abcd)], \
+        return [Item("c64", "lct", c4.values, c4.abcd)], \
             {"workload": f"cfg4 Fourier (0,1,-1,0) {c4.values.shape[0]}x1024 c64, Hermite mixtures seed 3",
              "rows": c4.values.shape[0], "n": 1024}
     if name == "cfg1":
         c1 = W.config1()
-        return [("c128", c1.values, c1.abcd)], {"workload": "cfg1 single LCT 1x1024 c128 (2,1,1,1)", "rows": 1, "n": 1024}
+        return [Item("c128", "lct", c1.values, c1.abcd)], {"workload": "cfg1 single LCT 1x1024 c128 (2,1,1,1)",
+                                                           "rows": 1, "n": 1024}
+    if name == "cfg3":
+        c3 = W.config3(rows=rows_override or 1024)
+        return [Item("c128", "mehler", c3.values, c3.extra["z"])], \
+            {"workload": f"cfg3 complex-z Mehler FrFT {c3.values.shape[0]}x16384 c128, r~U(.5,.99) seed 2",
+             "rows": c3.values.shape[0], "n": 16384}
+    if name == "cfg5":
+        n = rows_override or 16384
+        rl = n // world
+        field = W.config5_field(n=n, rows=rl, row_start=rank * rl)
+        # HBM: row pass read+write + column passes (2 round trips of the slab by the roofline model of
+        # SURVEY 8(d): 32 n^2 / G bytes per GPU); NVLink: 8 n^2 (G-1)/G^2 per GPU per direction
+        return [Item("c64", "lct2d", field, W.CONFIG5_ABCD, samples=n * n // world,
+                     alg_bytes=32 * n * n // world, extra={"n": n, "nvl_bytes": 8 * n * n * (world - 1) // world ** 2})], \
+            {"workload": f"cfg5 2-D Fresnel LCT {n}x{n} c64 (1,0.25,0,1) both axes, disk aperture seed 4",
+             "rows": n, "n": n}
     raise SystemExit(f"unknown config {name}")
 
 
 def samples_of(work):
-    return sum(v.shape[0] * v.shape[1] for _, v, _ in work)
+    return sum(it.samples for it in work)
 
 
 def bytes_of(work):
-    return sum(v.nbytes * 2 for _, v, _ in work)  # read + write of every sample
+    return sum(it.alg_bytes for it in work)
 
 
 # ---------------------------------------------------------------------------
 # CPU reference (oracle port) timing
 # ---------------------------------------------------------------------------
 def _cpu_worker(args):
-    abcd, vals = args
+    kind, p, vals = args
     from oracle import xft_oracle
 
     t0 = time.perf_counter()
-    xft_oracle.fast_lct_rows(abcd, vals.astype(np.complex128))
+    if kind == "mehler":  # the reference's only CPU path: the dense kernel matrix apply (512 outputs per row)
+        for z, f in zip(p, vals):
+            xft_oracle.mehler_apply(z, f.astype(np.complex128), rows_out=np.arange(0, f.shape[0], f.shape[0] // 512),
+                                    chunk=128)
+    else:  # 1-D rows (the 2-D transform is rows then columns of the same kernel)
+        xft_oracle.fast_lct_rows(p, vals.astype(np.complex128))
     return time.perf_counter() - t0
 
 
@@ -158,14 +189,14 @@ def cpu_reference(work, sample_rows: int, procs: int, pool=None):
 
     tasks = []
     total = 0
-    for _, v, p in work:
-        rows = min(sample_rows, v.shape[0])
-        pr = p if p.ndim == 1 else p[:rows]
+    for it in work:
+        v, p = it.values, np.asarray(it.params)
+        rows = min(sample_rows if it.kind != "mehler" else max(procs, sample_rows // 32), v.shape[0])
         block = max(1, rows // (procs * 4))
         for s in range(0, rows, block):
             e = min(rows, s + block)
-            tasks.append((pr if pr.ndim == 1 else pr[s:e], v[s:e]))
-        total += rows * v.shape[1]
+            tasks.append((it.kind, p if p.ndim <= 1 and it.kind != "mehler" else p[s:e], v[s:e]))
+        total += rows * (v.shape[1] if it.kind != "mehler" else 512)
     ex = pool if pool is not None else ProcessPoolExecutor(procs)
     try:
         if pool is None:
@@ -212,7 +243,7 @@ METRIC = "batched LCT Msamples/s at N=4096 c64/c128"
 
 
 def DTYPE_OF(work):
-    return "+".join(sorted({"c64" if v.dtype == np.complex64 else "c128" for _, v, _ in work}))
+    return "+".join(sorted({it.tag for it in work}))
 
 
 # ---------------------------------------------------------------------------
@@ -221,69 +252,116 @@ def DTYPE_OF(work):
 def run_ours(args, rank, world, local_rank):
     import torch
 
-    from paper_0912_1379_b200 import ops
+    from paper_0912_1379_b200 import lct2d as L2
+    from paper_0912_1379_b200 import mehler, ops
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    work, cfg = make_workload(args.config, args.rows)
-    nsets = 3  # rotate 3 input/output sets: every kernel reads cold data
-    sets = []
-    for _ in range(nsets):
-        s = []
-        for tag, v, p in work:
-            vin = torch.from_numpy(v).to(dev)
-            s.append((tag, vin, torch.empty_like(vin), torch.from_numpy(np.ascontiguousarray(p)).to(dev)))
-        sets.append(s)
+    work, cfg = make_workload(args.config, args.rows, rank, world)
+    nsets = 3  # rotate 3 input/output sets: every launch reads cold data (inputs > L2 for cfg2..5)
     stream = torch.cuda.Stream(dev)
 
     # validate once (reference order) outside the timed region
-    for _, v, p in work:
-        ops.validate_abcd_host(p)
+    for it in work:
+        if it.kind == "lct":
+            ops.validate_abcd_host(it.params)
 
-    # The step is captured once per buffer set as a CUDA graph (per-row
-    # coefficient kernel + transform kernel per dtype), so the timed loop is
-    # free of Python launch overhead: it replays graphs on one stream.
-    def capture(items):
-        with torch.cuda.stream(stream):  # warm (tables, attributes, allocator pools)
-            for tag, vin, vout, p in items:
-                ops.lct_rows(vin, p, out=vout, validate=False)
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for tag, vin, vout, p in items:
-                ops.lct_rows(vin, p, out=vout, validate=False)
-        return g
+    class State:
+        pass
 
-    step_graphs = [capture(sets[i]) for i in range(nsets)]
-    kern_graphs = [[capture([sets[i][k]]) for i in range(nsets)] for k in range(len(work))]
-    launches_per_step = 2 * len(work)  # coefficient kernel + transform kernel per dtype
+    def make_state(it):
+        st = State()
+        st.vin = torch.from_numpy(it.values).to(dev)
+        st.vout = torch.empty_like(st.vin)
+        st.p = torch.from_numpy(np.ascontiguousarray(it.params)).to(dev) if it.kind == "lct" else it.params
+        if it.kind == "lct2d":
+            if world == 1:
+                st.ws = torch.empty_like(st.vin)
+            else:
+                rl, n = st.vin.shape
+                st.bufs = (torch.empty((world, rl, n // world), dtype=st.vin.dtype, device=dev),
+                           torch.empty((world, rl, n // world), dtype=st.vin.dtype, device=dev))
+        return st
+
+    def launch(it, st):
+        if it.kind == "lct":
+            ops.lct_rows(st.vin, st.p, out=st.vout, validate=False)
+        elif it.kind == "mehler":
+            mehler.mehler_rows(st.vin, st.p, out=st.vout)
+        elif world == 1:
+            L2.lct2d(st.vin, st.p, st.p, out=st.vout, workspace=st.ws)
+        else:
+            L2.lct2d_sharded(st.vin, st.p, st.p, buffers=st.bufs)
+
+    sets = [[make_state(it) for it in work] for _ in range(nsets)]
+    # Mehler plans upload per-row tables from the host and the sharded 2-D pass calls
+    # NCCL through torch.distributed: those steps are launched directly; everything
+    # else is captured as CUDA graphs so the timed loop has no Python launch overhead.
+    capturable = all(it.kind == "lct" or (it.kind == "lct2d" and world == 1) for it in work)
+    chunk = max(1, min(10, args.steps))
+
+    def runner(item_idx):
+        """callable(n_steps) that launches n steps on `stream` (all items, or one item)."""
+        idx = range(len(work)) if item_idx is None else [item_idx]
+        if not capturable:
+            def run(nsteps):
+                for i in range(nsteps):
+                    for k in idx:
+                        launch(work[k], sets[i % nsets][k])
+            return run
+        graphs = {}
+        per_set = [[(work[k], sets[i][k]) for k in idx] for i in range(nsets)]
+
+        def graph(reps):
+            if reps not in graphs:
+                with torch.cuda.stream(stream):
+                    for i in range(nsets):
+                        for it, st in per_set[i]:
+                            launch(it, st)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for r in range(reps):
+                        for it, st in per_set[r % nsets]:
+                            launch(it, st)
+                graphs[reps] = g
+            return graphs[reps]
+
+        graph(chunk)
+        if args.steps % chunk:
+            graph(args.steps % chunk)
+
+        def run(nsteps):
+            for _ in range(nsteps // chunk):
+                graph(chunk).replay()
+            if nsteps % chunk:
+                graph(nsteps % chunk).replay()
+        return run
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
-    def timed(graphs, n):
+    def timed(run, n):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for i in range(n):
-            graphs[i % nsets].replay()
+        run(n)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         return e0.elapsed_time(e1)
 
     with torch.cuda.stream(stream):
-        for i in range(args.warmup):
-            step_graphs[i % nsets].replay()
+        step_run = runner(None)
+        kern_runs = [runner(k) for k in range(len(work))]
+        step_run(max(args.warmup, 3))  # warm-up (graphs for the remainder are captured here too)
         torch.cuda.synchronize()
-        # per-kernel averages (same replay scheme, one dtype at a time)
-        kern_ms = [timed(kern_graphs[k], args.steps) / args.steps for k in range(len(work))]
-        # main timed region: K steps bracketed by barrier + synchronize
+        kern_ms = [timed(kern_runs[k], args.steps) / args.steps for k in range(len(work))]
         with ClockSampler(local_rank) as clk:
-            total_ms = timed(step_graphs, args.steps)
+            total_ms = timed(step_run, args.steps)
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -291,44 +369,62 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = total_ms / args.steps
     samples = samples_of(work)
     value = world * samples / (ms_per_step * 1e-3) / 1e6
+    launches_per_step = sum({"lct": 2, "mehler": 2, "lct2d": 4}[it.kind] for it in work)
 
-    # end-to-end through the public host-buffer API
+    # end-to-end through the public host-buffer API: pinned host in, result back on the host
     e2e_steps = max(2, min(args.steps, args.e2e_steps))
     pinned = []
-    for tag, v, p in work:
-        hin = torch.from_numpy(v).pin_memory()
+    for it in work:
+        hin = torch.from_numpy(it.values).pin_memory()
         hout = torch.empty_like(hin).pin_memory()
-        pinned.append((hin.numpy(), hout.numpy(), p))
-    for hin, hout, p in pinned:
-        ops.lct_host(hin, p, out=hout)
+        pinned.append((it, hin, hout))
+
+    def e2e_once():
+        for it, hin, hout in pinned:
+            if it.kind == "lct":
+                ops.lct_host(hin.numpy(), it.params, out=hout.numpy())  # xft_lct_host: chunked H2D/kernel/D2H
+            else:
+                st = sets[0][work.index(it)]
+                st.vin.copy_(hin, non_blocking=True)
+                with torch.cuda.stream(torch.cuda.current_stream(dev)):
+                    launch(it, st)
+                res = st.vout if it.kind != "lct2d" or world == 1 else st.bufs[1]
+                hout.view(-1)[:res.numel()].copy_(res.view(-1), non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+
+    e2e_once()
     barrier()
     te = time.perf_counter()
     for _ in range(e2e_steps):
-        for hin, hout, p in pinned:
-            ops.lct_host(hin, p, out=hout)
+        e2e_once()
     e2e_dt = time.perf_counter() - te
     if world > 1:
         t = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_dt = float(t.item())
     e2e_value = world * samples * e2e_steps / e2e_dt / 1e6
-    h2d = sum(h.nbytes + p.nbytes for h, _, p in pinned)
-    d2h = sum(o.nbytes for _, o, _ in pinned)
+    h2d = sum(h.nbytes for _, h, _ in pinned) + sum(np.asarray(it.params).nbytes for it in work)
+    d2h = sum(o.nbytes for _, _, o in pinned)
 
     if rank != 0:
         return
     peak, peak_kind = load_peaks()
     traffic = load_traffic()
     per = {}
-    for k, (tag, v, p) in enumerate(work):
-        alg_bytes = v.nbytes * 2
-        ach = alg_bytes / (kern_ms[k] * 1e-3) / 1e9
-        per[tag] = {"kernel_ms": kern_ms[k], "Msamples_per_s": v.size / (kern_ms[k] * 1e-3) / 1e6,
-                    "achieved_GBps": ach, "frac": ach / peak, "alg_bytes_per_launch": alg_bytes,
-                    "traffic": traffic.get(f"{args.config}_{tag}")}
+    for k, it in enumerate(work):
+        ach = it.alg_bytes / (kern_ms[k] * 1e-3) / 1e9
+        per[it.tag] = {"kernel_ms": kern_ms[k], "Msamples_per_s": it.samples / (kern_ms[k] * 1e-3) / 1e6,
+                       "achieved_GBps": ach, "frac": ach / peak, "alg_bytes_per_launch": it.alg_bytes,
+                       "traffic": traffic.get(f"{args.config}_{it.tag}")}
+        if "nvl_bytes" in it.extra and world > 1:
+            t_roof = it.alg_bytes / (peak * 1e9) + it.extra["nvl_bytes"] / 900e9
+            per[it.tag]["hbm_nvlink_serial_roofline_ms"] = t_roof * 1e3
+            per[it.tag]["frac_of_hbm_nvlink_roofline"] = t_roof * 1e3 / kern_ms[k]
     dom = max(per, key=lambda t: per[t]["kernel_ms"])
+    kname = {"lct": "xft_pipe_kernel", "mehler": "xft_blue_kernel + xft_tile_kernel",
+             "lct2d": "xft_pipe_kernel + xft_tile_kernel"}[work[[it.tag for it in work].index(dom)].kind]
     roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
-            "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"xft_pipe_kernel {dom}",
+            "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"{kname} {dom}",
             "peak_source": peak_kind,
             "step_achieved": bytes_of(work) / (ms_per_step * 1e-3) / 1e9}
 
@@ -337,17 +433,20 @@ def run_ours(args, rank, world, local_rank):
         procs = len(os.sched_getaffinity(0))
         v, total, dt = cpu_reference(work, args.cpu_rows, procs)
         cpu = {"value": v, "unit": "Msamples/s", "cores": procs, "kind": "port",
-               "sample": f"{args.cpu_rows} rows per dtype of the same batch ({total} samples, {dt:.1f} s), "
-                         f"oracle/xft_oracle.py fast_lct_rows in a {procs}-process pool"}
+               "sample": f"{args.cpu_rows} rows per item of the same batch ({total} samples, {dt:.1f} s), "
+                         f"oracle/xft_oracle.py in a {procs}-process pool"}
     line = {
         "metric": METRIC, "value": value, "unit": "Msamples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded, BASELINE config draw order)",
         "config": dict(cfg, l2="3 rotating input/output sets; each launch streams >= 2x L2 of cold data",
-                       parallelism=f"batch-sharded x{world}, no collective"),
+                       parallelism=(f"batch-sharded x{world}, no collective" if args.config != "cfg5"
+                                    else f"row-sharded x{world}, one NCCL all_to_all_single"),
+                       timing="CUDA graphs" if capturable else "direct launches"),
         "roofline": roof, "per_dtype": per, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "Msamples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "steps": e2e_steps, "api": "paper_0912_1379_b200.ops.lct_host -> xft_lct_host"},
+                "steps": e2e_steps, "api": "ops.lct_host -> xft_lct_host" if work[0].kind == "lct"
+                else "pinned H2D + public op + D2H"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }

@@ -108,24 +108,30 @@ def config4_closed_form(coeffs: np.ndarray, n: int = 1024) -> np.ndarray:
     return (coeffs * phase) @ psi_y
 
 
-def config5_field(n: int = 16384, rows=None, out=None) -> np.ndarray:
+def config5_field(n: int = 16384, rows=None, out=None, row_start: int = 0) -> np.ndarray:
     """Random-phase disk aperture, radius 0.3 * (x[-1]-x[0]), phase ~ U(0, 2pi) [n, n], seed 4; c64.
 
     Drawn row block by row block (the uniform stream is consumed in the same
-    row-major order as one (n, n) draw).  ``rows`` limits to the first rows.
+    row-major order as one (n, n) draw).  ``row_start``/``rows`` select a row
+    shard: the generator is advanced past the earlier rows (one 64-bit draw
+    per uniform double), so every shard is bit-identical to the same rows of
+    the full draw.
     """
     x = asymptotic_zeros(n).nodes
     extent = x[-1] - x[0]
     R = 0.3 * extent
-    nrows = n if rows is None else rows
+    nrows = (n - row_start) if rows is None else rows
     field = out if out is not None else np.empty((nrows, n), dtype=np.complex64)
     rng = np.random.default_rng(4)
+    if row_start:
+        rng.bit_generator.advance(row_start * n)
     blk = 256
     x2 = x * x
     for s in range(0, nrows, blk):
         e = min(s + blk, nrows)
         phase = rng.uniform(0.0, 2 * math.pi, (e - s, n))
-        inside = (x2[s:e, None] + x2[None, :]) <= R * R
+        gs, ge = row_start + s, row_start + e
+        inside = (x2[gs:ge, None] + x2[None, :]) <= R * R
         field[s:e] = (inside * np.exp(1j * phase)).astype(np.complex64)
     return field
 

@@ -101,3 +101,11 @@ def test_norm_identity():
     lhs = np.sum(np.abs(v) ** 2, axis=1)
     rhs = math.pi / (4 * np.abs(P[:, 1])) * np.sum(np.abs(f) ** 2, axis=1)
     assert np.allclose(lhs, rhs, rtol=1e-12)
+
+
+def test_config5_shards_are_rows_of_the_full_draw():
+    from paper_0912_1379_b200 import workloads
+
+    full = workloads.config5_field(n=128)
+    part = workloads.config5_field(n=128, rows=32, row_start=64)
+    assert np.array_equal(full[64:96], part)
