@@ -74,7 +74,7 @@ struct PipeShape {
   static constexpr int ROWS = TR >= TARGET ? 1 : (TARGET / TR > 64 ? 64 : TARGET / TR);
   static constexpr int MINB0 = C64 ? XFT_C64_MINB : XFT_C128_MINB;
   static constexpr size_t TILE_BYTES = size_t(ROWS) * (size_t(1) << L) * sizeof(C);
-  static constexpr size_t STATIC = 2 * ROWS * (C64 ? sizeof(Coef64) : sizeof(Coef128)) + 256;
+  static constexpr size_t STATIC = (ROWS >= 128 ? ROWS : 128) * (C64 ? sizeof(Coef64) : sizeof(Coef128)) + 256;
   static constexpr size_t TAB = C64 ? 0 : XFT_C128_TABCOPIES * 256 * 16;
   // resident CTAs per SM: requested, capped by threads (2048/SM) and by one stage of smem
   static constexpr int MINB_T = 65536 / (TR * ROWS * 64);  // keep >= 64 registers per thread
@@ -112,22 +112,10 @@ int launch_pipe(const LaunchArgs& a) {
   kc.cnred = (long long)(((__int128)((1 << L) - 1) * ((1 << L) - 1)) % (4 * (__int128)(1 << L)));
   kc.log2n = L;
   kc.flags = a.flags;
-  using Coef = typename Cfg::Coef;
-  Coef* coefs = nullptr;
-  int per_row = 0;
-  if constexpr (MODE == MODE_LCT) {
-    // per-row coefficients (divisions, branch cuts, phase offsets) once per row,
-    // streamed into shared memory by the same TMA as the rows
-    per_row = (a.abcd != nullptr && a.stride != 0) ? 1 : 0;
-    const long long nco = per_row ? a.batch : 1;
-    if (cudaMallocAsync((void**)&coefs, sizeof(Coef) * nco, a.st) != cudaSuccess) return XFT_ECUDA;
-    xft_coef_kernel<Coef><<<(unsigned)((nco + 127) / 128), 128, 0, a.st>>>(coefs, nco, a.abcd, a.stride, a.uni, kc);
-  }
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
-      static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, coefs, per_row,
+      static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
       static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc, a.seg_log2w,
       a.seg_stride);
-  if (coefs) cudaFreeAsync(coefs, a.st);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
 }
 

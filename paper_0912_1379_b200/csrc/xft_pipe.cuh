@@ -68,9 +68,8 @@ static __constant__ double kStepPi16[16] = {
 // ---------------------------------------------------------------------------
 // per-row coefficients
 // ---------------------------------------------------------------------------
-// Computed once per row by xft_coef_kernel (a [B] array in device memory) and
-// brought into shared memory by the same bulk TMA as the row data.  Sizes are
-// multiples of 16 bytes (bulk-copy granularity).
+// Computed once per row inside the row kernel, by all threads of a CTA for
+// the next CH tiles at a time, into shared memory.
 struct __align__(16) Coef64 {
   unsigned long long dq_in, dq_out;  // Q0.64 turns per unit k'^2 (chirp rates)
   uint32_t gq;                       // top 32 bits of arg G in turns
@@ -475,23 +474,15 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const O
 }
 
 // ---------------------------------------------------------------------------
-// the kernel.  Thread 0 keeps STAGES-1 tile loads in flight (bulk TMA of the
-// rows and of their precomputed coefficients onto one mbarrier per stage);
-// every thread transforms.  The next load is issued right after the first
+// the kernel.  Thread 0 keeps STAGES-1 tile loads in flight (bulk TMA onto
+// one mbarrier per stage); every thread transforms.  The next load is issued right after the first
 // exchange barrier of the current tile, i.e. once every thread has finished
 // the previous tile and the oldest stage is free.
 // ---------------------------------------------------------------------------
-template <class Coef>
-__global__ void xft_coef_kernel(Coef* __restrict__ out, long long rows, const double* __restrict__ abcd,
-                                long long stride, Abcd uni, RowConst kc) {
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < rows) make_coef(out[r], abcd ? abcd + r * stride : nullptr, uni, kc);
-}
-
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restrict__ out, long long batch,
-                const typename Cfg::Coef* __restrict__ coefs, int coef_per_row, const typename Cfg::C* __restrict__ tw,
+                const double* __restrict__ abcd, long long abcd_stride, Abcd uni, const typename Cfg::C* __restrict__ tw,
                 const typename Cfg::C* __restrict__ ptab, const void* __restrict__ gtab, double2 cn, RowConst kc,
                 int seg_log2w, long long seg_stride) {
   using C = typename Cfg::C;
@@ -499,7 +490,10 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   constexpr int N = Cfg::N, ROWS = Cfg::ROWS, S = Cfg::STAGES;
   extern __shared__ __align__(128) unsigned char xft_smem[];
   __shared__ __align__(8) uint64_t bars[S];
-  __shared__ Coef coefbuf[Cfg::MODE == MODE_LCT ? S : 1][Cfg::MODE == MODE_LCT ? ROWS : 1];
+  // per-row coefficients of the next CH tiles of this CTA, computed by all
+  // threads together once per CH tiles (one make_coef latency per chunk)
+  constexpr int CH = Cfg::MODE == MODE_LCT ? (ROWS >= 128 ? 1 : 128 / ROWS < 32 ? 128 / ROWS : 32) : 1;
+  __shared__ Coef coeft[CH][Cfg::MODE == MODE_LCT ? ROWS : 1];
 
   C* stage0 = reinterpret_cast<C*>(xft_smem);
   void* tab = xft_smem + size_t(S) * Cfg::TILE * sizeof(C);
@@ -515,12 +509,16 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     fence_proxy_async_smem();
     const long long rows = batch - t * ROWS < ROWS ? batch - t * ROWS : ROWS;
     const uint32_t bytes = (uint32_t)(rows * N * sizeof(C));
-    uint32_t cbytes = 0;
-    if constexpr (Cfg::MODE == MODE_LCT) cbytes = (uint32_t)((coef_per_row ? rows : 1) * sizeof(Coef));
-    mbar_arrive_expect_tx(&bars[st], bytes + cbytes);
+    mbar_arrive_expect_tx(&bars[st], bytes);
     tma_load_1d(stage0 + size_t(st) * Cfg::TILE, in + t * Cfg::TILE, bytes, &bars[st]);
-    if constexpr (Cfg::MODE == MODE_LCT)
-      tma_load_1d(&coefbuf[st][0], coefs + (coef_per_row ? t * ROWS : 0), cbytes, &bars[st]);
+  };
+  auto fill_coefs = [&](long long first_tile) {  // tiles first_tile + q*G, q < CH
+    if constexpr (Cfg::MODE == MODE_LCT) {
+      for (int idx = threadIdx.x; idx < CH * ROWS; idx += Cfg::THREADS) {
+        const long long row = (first_tile + (long long)(idx / ROWS) * G) * ROWS + idx % ROWS;
+        if (row < batch) make_coef(coeft[idx / ROWS][idx % ROWS], abcd ? abcd + row * abcd_stride : nullptr, uni, kc);
+      }
+    }
   };
 
   // ---- prologue ----
@@ -543,10 +541,17 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
 
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int st = it % S;
+    if constexpr (Cfg::MODE == MODE_LCT) {
+      if (it % CH == 0) {
+        __syncthreads();  // the previous chunk's coefficients are no longer read
+        fill_coefs(tile);
+        __syncthreads();
+      }
+    }
     mbar_wait(&bars[st], (uint32_t)((it / S) & 1));
     C* rs = stage0 + size_t(st) * Cfg::TILE + size_t(lrow) * N;
     Coef rc;
-    if constexpr (Cfg::MODE == MODE_LCT) rc = coefbuf[st][coef_per_row ? lrow : 0];
+    if constexpr (Cfg::MODE == MODE_LCT) rc = coeft[it % CH][lrow];
 
     C v[Cfg::E];
     if constexpr (XFT_SKELETON) {
