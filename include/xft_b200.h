@@ -131,7 +131,7 @@ int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, i
 
 /* Row LCT (one quadruple, host) written in the all-to-all send layout of the
  * sharded 2-D transform: segment g (2^seg_log2w samples) of row r is stored at
- * out + g*seg_stride + r*2^seg_log2w.  seg_stride >= batch * 2^seg_log2w. */
+ * out + g*seg_stride + r*2^seg_log2w (seg_stride >= batch * 2^seg_log2w). */
 int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd_host,
                         int seg_log2w, int64_t seg_stride, void* stream);
 

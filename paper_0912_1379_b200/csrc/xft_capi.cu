@@ -72,17 +72,18 @@ struct PipeShape {
   static constexpr int TR = (1 << L) / E;
   static constexpr int TARGET = C64 ? XFT_C64_TARGET : XFT_C128_TARGET;  // threads per CTA
   static constexpr int ROWS = TR >= TARGET ? 1 : (TARGET / TR > 64 ? 64 : TARGET / TR);
-  static constexpr int MINB0 = C64 ? XFT_C64_MINB : XFT_C128_MINB;
+  // c64 rows up to 1024: two resident CTAs with a 3-deep ring measured best (cfg4); longer rows: 4 CTAs
+  static constexpr int MINB0 = C64 ? (L <= 10 ? 2 : XFT_C64_MINB) : XFT_C128_MINB;
   static constexpr size_t TILE_BYTES = size_t(ROWS) * (size_t(1) << L) * sizeof(C);
   static constexpr size_t STATIC = (ROWS >= 128 ? ROWS : 128) * (C64 ? sizeof(Coef64) : sizeof(Coef128)) + 256;
-  static constexpr size_t TAB = C64 ? 0 : XFT_C128_TABCOPIES * 256 * 16;
+  static constexpr size_t TAB = C64 ? 0 : XFT_C128_TABCOPIES * 256 * 16;  // (XFT_C128_TABCOPIES from xft_pipe.cuh)
   // resident CTAs per SM: requested, capped by threads (2048/SM) and by one stage of smem
   static constexpr int MINB_T = 65536 / (TR * ROWS * 64);  // keep >= 64 registers per thread
   static constexpr int MINB_S = int((226 * 1024) / (TILE_BYTES + TAB + STATIC + 1024));
   static constexpr int MINB1 = MINB0 < MINB_T ? MINB0 : MINB_T;
   static constexpr int MINB = (MINB1 < MINB_S ? MINB1 : MINB_S) < 1 ? 1 : (MINB1 < MINB_S ? MINB1 : MINB_S);
   static constexpr size_t BUDGET = (226 * 1024) / MINB - 1024 - STATIC - TAB;
-  static constexpr int MAXST = C64 ? XFT_C64_MAXST : XFT_C128_MAXST;
+  static constexpr int MAXST = C64 ? (L <= 10 ? 3 : XFT_C64_MAXST) : XFT_C128_MAXST;
   static constexpr int STAGES = BUDGET / TILE_BYTES >= MAXST ? MAXST : (BUDGET / TILE_BYTES >= 2 ? 2 : 1);
 };
 
@@ -164,7 +165,7 @@ int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64
   LaunchArgs a{in, out, (long long)batch, abcd, (long long)stride, uni, {}, flags, st};
   a.seg_log2w = seg_log2w;
   a.seg_stride = seg_stride;
-  if (seg_stride && (seg_log2w > l || mode != MODE_LCT)) return XFT_EPARAM;
+  if (seg_stride && (seg_log2w < 0 || seg_log2w > l || mode != MODE_LCT)) return XFT_EPARAM;
   int rc = get_tables(n, dtype, &a.tb);
   if (rc) return rc;
   LaunchFn fn = nullptr;
@@ -318,7 +319,7 @@ int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int
                         int seg_log2w, int64_t seg_stride, void* stream) {
   int rc = xft_validate_lct_params(abcd_host, 1, 0, 1, 1e-10, nullptr);
   if (rc) return rc;
-  if (seg_stride < (int64_t)batch << seg_log2w) return XFT_ESHAPE;
+  if (seg_log2w < 0 || seg_stride < (int64_t)batch << seg_log2w) return XFT_ESHAPE;
   const Abcd u{abcd_host[0], abcd_host[1], abcd_host[2], abcd_host[3]};
   return run_rows(MODE_LCT, -1, in, out, batch, n, dtype, nullptr, 0, u, 0, static_cast<cudaStream_t>(stream),
                   seg_log2w, seg_stride);

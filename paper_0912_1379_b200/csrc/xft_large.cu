@@ -365,41 +365,45 @@ struct PostMehler {
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
-template <class C, int LOGL, bool LC, bool SC, int SIGN, class Op>
+template <class C, int LOGL, bool LC, bool SC, int SIGN, int W, class Op>
 int launch_tile(long long ntiles, const Op& op, cudaStream_t st) {
   constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
-  constexpr int W = tile_w<C>();
   constexpr int E = tile_e<C>(LOGL);
   constexpr int T = W * ((1 << LOGL) / E);
   constexpr size_t SM = tile_smem<C, LOGL, W>();
-  auto kern = xft_tile_kernel<C, LOGL, E, W, LC, SC, SIGN, Op>;
-  Tables tb;
-  int rc = get_tables(int64_t(1) << LOGL, dtype, &tb, E);
-  if (rc) return rc;
-  if (SM > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM) != cudaSuccess)
-    return XFT_ECUDA;
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, SM);
-  const long long cap = (long long)sms * (occ < 1 ? 1 : occ);
-  kern<<<(unsigned)(ntiles < cap ? ntiles : cap), T, SM, st>>>(ntiles, op, static_cast<const C*>(tb.tw));
-  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+  if constexpr (T > 1024 || SM > 200 * 1024) {
+    return XFT_ENOTSUP;  // tile too wide for this line length (callers fall back to narrower tiles)
+  } else {
+    auto kern = xft_tile_kernel<C, LOGL, E, W, LC, SC, SIGN, Op>;
+    Tables tb;
+    int rc = get_tables(int64_t(1) << LOGL, dtype, &tb, E);
+    if (rc) return rc;
+    if (SM > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM) != cudaSuccess)
+      return XFT_ECUDA;
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, SM);
+    const long long cap = (long long)sms * (occ < 1 ? 1 : occ);
+    kern<<<(unsigned)(ntiles < cap ? ntiles : cap), T, SM, st>>>(ntiles, op, static_cast<const C*>(tb.tw));
+    return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+  }
 }
 
 constexpr int LMIN = 6, LMAX = 10;  // per-pass lengths 64 .. 1024  =>  M up to 2^20
 
-template <class C, bool LC, bool SC, int SIGN, class Op, int... Ls>
+template <class C, bool LC, bool SC, int SIGN, int W, class Op, int... Ls>
 int tile_dispatch(int l, long long ntiles, const Op& op, cudaStream_t st, std::integer_sequence<int, Ls...>) {
   int rc = XFT_ENOTSUP;
-  ((l == Ls + LMIN ? (rc = launch_tile<C, Ls + LMIN, LC, SC, SIGN, Op>(ntiles, op, st), 0) : 0), ...);
+  ((l == Ls + LMIN ? (rc = launch_tile<C, Ls + LMIN, LC, SC, SIGN, W, Op>(ntiles, op, st), 0) : 0), ...);
   return rc;
 }
 
-template <class C, bool LC, bool SC, int SIGN, class Op>
+template <class C, bool LC, bool SC, int SIGN, class Op, int W = tile_w<C>()>
 int tile(int l, long long ntiles, const Op& op, cudaStream_t st) {
   if (l < LMIN || l > LMAX) return XFT_ENOTSUP;
-  return tile_dispatch<C, LC, SC, SIGN, Op>(l, ntiles, op, st, std::make_integer_sequence<int, LMAX - LMIN + 1>{});
+  return tile_dispatch<C, LC, SC, SIGN, W, Op>(l, ntiles, op, st, std::make_integer_sequence<int, LMAX - LMIN + 1>{});
 }
 
 // samples outside a Mehler row's window: exact zeros
@@ -750,8 +754,8 @@ ColChirp col_chirp(const double* abcd, int64_t R, int bare) {
 }
 
 template <class C>
-int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, const double* abcd, int bare,
-             cudaStream_t st) {
+int lct_cols_narrow(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, const double* abcd,
+                    int bare, cudaStream_t st) {
   constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
   constexpr int W = tile_w<C>();
   if (ncols % W) return XFT_ENOTSUP;
@@ -773,6 +777,36 @@ int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int6
   if ((rc = tile<C, true, true, -1>(sh.l1, (long long)R2 * (ncols / W), op1, st))) return rc;
   OpColLct2<C> op2{static_cast<const C*>(ws), static_cast<C*>(out), ld, W, (int)ncols, R1, R2, k, cptab};
   return tile<C, true, true, -1>(sh.l2, (long long)R1 * (ncols / W), op2, st);
+}
+
+#ifndef XFT_COLW
+#define XFT_COLW 4  // column tiles: 512 contiguous bytes per access (DRAM page locality)
+#endif
+template <class C>
+int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, const double* abcd, int bare,
+             cudaStream_t st) {
+  constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
+  constexpr int W = tile_w<C>() * XFT_COLW;
+  const int l = log2_of(R);
+  // wide tiles for the two-pass (four-step) heights; one-pass heights use 128-byte tiles
+  if (ncols % W || l <= LMAX) return lct_cols_narrow<C>(in, out, ws, R, ncols, ld, abcd, bare, st);
+  const ColChirp k = col_chirp(abcd, R, bare);
+  const double2 *ptab = nullptr, *cptab = nullptr;
+  int rc = boundary_tables(R, &ptab, &cptab);
+  if (rc) return rc;
+  if (l <= LMAX) {
+    OpColLctOne<C> op{static_cast<const C*>(in), static_cast<C*>(out), ld, W, k, ptab, cptab};
+    return tile<C, true, true, -1, OpColLctOne<C>, W>(l, ncols / W, op, st);
+  }
+  const Shape sh = split(l);
+  const int R1 = 1 << sh.l1, R2 = 1 << sh.l2;
+  const void* twr = nullptr;
+  if ((rc = natural_twiddles(R, dtype, &twr))) return rc;
+  OpColLct1<C> op1{static_cast<const C*>(in), static_cast<C*>(ws), ld, W, (int)ncols, R2, k, ptab,
+                   static_cast<const C*>(twr)};
+  if ((rc = tile<C, true, true, -1, OpColLct1<C>, W>(sh.l1, (long long)R2 * (ncols / W), op1, st))) return rc;
+  OpColLct2<C> op2{static_cast<const C*>(ws), static_cast<C*>(out), ld, W, (int)ncols, R1, R2, k, cptab};
+  return tile<C, true, true, -1, OpColLct2<C>, W>(sh.l2, (long long)R1 * (ncols / W), op2, st);
 }
 
 }  // namespace

@@ -35,7 +35,7 @@
 #define XFT_SKELETON 0  // tuning only: 1 = exchanges without math, 2 = pure copy
 #endif
 #ifndef XFT_C128_TABCOPIES
-#define XFT_C128_TABCOPIES 8
+#define XFT_C128_TABCOPIES 1
 #endif
 
 namespace xftb {

@@ -22,7 +22,7 @@ namespace xftb {
 template <class C, int LOGL, int E, int W, bool LOAD_COL, bool STORE_COL, int SIGN, class Op>
 __global__ void __launch_bounds__(W*((1 << LOGL) / E))
 xft_tile_kernel(long long ntiles, Op op, const C* __restrict__ tw) {
-  constexpr int L = 1 << LOGL, TR = L / E, T = W * TR;
+  constexpr int L = 1 << LOGL, TR = L / E;
   using Fwd = PipeCfg<C, LOGL, E, MODE_DFT, SIGN, W, 1, 1>;
   using Inv = PipeCfg<C, LOGL, E, MODE_DFT, -SIGN, W, 1, 1>;
   constexpr int LS = L + 1;  // padded line stride: adjacent lines start in different banks

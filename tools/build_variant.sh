@@ -6,6 +6,10 @@ OUT=../../tune/libxft_$1.so
 B=../../tune/build_$1
 mkdir -p $B
 A="-gencode arch=compute_100a,code=sm_100a"
-nvcc -O3 -std=c++17 -lineinfo $A -Xcompiler -fPIC --expt-relaxed-constexpr $2 -c xft_capi.cu -o $B/capi.o
-nvcc -O3 -std=c++17 -lineinfo $A -Xcompiler -fPIC --expt-relaxed-constexpr $2 -c xft_tables.cu -o $B/tables.o
-nvcc $A -shared -o $OUT $B/capi.o $B/tables.o -lcudart
+OBJS=""
+for f in *.cu; do
+  nvcc -O3 -std=c++17 -lineinfo $A -Xcompiler -fPIC --expt-relaxed-constexpr $2 -c $f -o $B/${f%.cu}.o &
+  OBJS="$OBJS $B/${f%.cu}.o"
+done
+wait
+nvcc $A -shared -o $OUT $OBJS -lcudart
