@@ -34,7 +34,12 @@ namespace {
 const long double PI_L = 3.141592653589793238462643383279502884L;
 
 template <class C> constexpr int tile_w() { return sizeof(C) == 8 ? 16 : 8; }    // 128-byte lines
-template <class C> constexpr int tile_e(int l) { return l >= 8 ? (sizeof(C) == 8 ? 16 : 8) : 8; }
+#ifndef XFT_TILE_E7
+#define XFT_TILE_E7 8
+#endif
+template <class C> constexpr int tile_e(int l) {
+  return l >= 8 ? (sizeof(C) == 8 ? 16 : 8) : (l == 7 && sizeof(C) == 8 ? XFT_TILE_E7 : 8);
+}
 
 // natural twiddles e^{-2 pi i m / M}, m < M, per (device, M, dtype)
 std::mutex g_mu;
@@ -670,7 +675,7 @@ struct OpColLct1 {  // four-step pass 1: DFT over r1 for the line (r2, c); twidd
   static constexpr bool MID = false;
   const C* in;
   C* scr;
-  long long ld;
+  long long ld, lds;  // row strides of the slab and of the scratch
   int W, ncols, R2;
   ColChirp k;
   const double2* ptab;
@@ -684,7 +689,7 @@ struct OpColLct1 {  // four-step pass 1: DFT over r1 for the line (r2, c); twidd
   __device__ void store(long long tile, int w, int a, C v) const {
     const int cb = ncols / W;
     const long long r2 = tile / cb, c = (tile % cb) * W + w;
-    scr[((long long)a * R2 + r2) * ld + c] = cmul(v, twr[(long long)a * r2]);
+    scr[((long long)a * R2 + r2) * lds + c] = cmul(v, twr[(long long)a * r2]);
   }
 };
 
@@ -693,14 +698,14 @@ struct OpColLct2 {  // pass 2: DFT over r2 for the line (k1, c); natural row j =
   static constexpr bool MID = false;
   const C* scr;
   C* out;
-  long long ld;
+  long long ld, lds;
   int W, ncols, R1, R2;
   ColChirp k;
   const double2* cptab;
   __device__ C load(long long tile, int w, int a) const {
     const int cb = ncols / W;
     const long long k1 = tile / cb, c = (tile % cb) * W + w;
-    return scr[(k1 * R2 + a) * ld + c];
+    return scr[(k1 * R2 + a) * lds + c];
   }
   __device__ void store(long long tile, int w, int a, C v) const {
     const int cb = ncols / W;
@@ -772,13 +777,16 @@ int lct_cols_narrow(const void* in, void* out, void* ws, int64_t R, int64_t ncol
   const int R1 = 1 << sh.l1, R2 = 1 << sh.l2;
   const void* twr = nullptr;
   if ((rc = natural_twiddles(R, dtype, &twr))) return rc;
-  OpColLct1<C> op1{static_cast<const C*>(in), static_cast<C*>(ws), ld, W, (int)ncols, R2, k, ptab,
+  OpColLct1<C> op1{static_cast<const C*>(in), static_cast<C*>(ws), ld, ld, W, (int)ncols, R2, k, ptab,
                    static_cast<const C*>(twr)};
   if ((rc = tile<C, true, true, -1>(sh.l1, (long long)R2 * (ncols / W), op1, st))) return rc;
-  OpColLct2<C> op2{static_cast<const C*>(ws), static_cast<C*>(out), ld, W, (int)ncols, R1, R2, k, cptab};
+  OpColLct2<C> op2{static_cast<const C*>(ws), static_cast<C*>(out), ld, ld, W, (int)ncols, R1, R2, k, cptab};
   return tile<C, true, true, -1>(sh.l2, (long long)R1 * (ncols / W), op2, st);
 }
 
+#ifndef XFT_COLSLAB_MB
+#define XFT_COLSLAB_MB 4096  // L2-resident scratch per column slab (4096: one slab; smaller slabs measured slower)
+#endif
 #ifndef XFT_COLW
 #define XFT_COLW 4  // column tiles: 512 contiguous bytes per access (DRAM page locality)
 #endif
@@ -802,11 +810,22 @@ int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int6
   const int R1 = 1 << sh.l1, R2 = 1 << sh.l2;
   const void* twr = nullptr;
   if ((rc = natural_twiddles(R, dtype, &twr))) return rc;
-  OpColLct1<C> op1{static_cast<const C*>(in), static_cast<C*>(ws), ld, W, (int)ncols, R2, k, ptab,
-                   static_cast<const C*>(twr)};
-  if ((rc = tile<C, true, true, -1, OpColLct1<C>, W>(sh.l1, (long long)R2 * (ncols / W), op1, st))) return rc;
-  OpColLct2<C> op2{static_cast<const C*>(ws), static_cast<C*>(out), ld, W, (int)ncols, R1, R2, k, cptab};
-  return tile<C, true, true, -1, OpColLct2<C>, W>(sh.l2, (long long)R1 * (ncols / W), op2, st);
+  // column slabs whose [R][slab] scratch fits in L2: the intermediate of the
+  // two passes never goes to HBM, so the column transform costs one HBM round trip
+  int64_t slab = ((int64_t)XFT_COLSLAB_MB << 20) / (R * (int64_t)sizeof(C));
+  slab = slab < W ? W : (slab / W) * W;
+  if (slab > ncols) slab = ncols;
+  for (int64_t c0 = 0; c0 < ncols; c0 += slab) {
+    const int64_t cw = ncols - c0 < slab ? ncols - c0 : slab;
+    if (cw % W) return lct_cols_narrow<C>(static_cast<const C*>(in) + c0, static_cast<C*>(out) + c0, ws, R, cw, ld,
+                                          abcd, bare, st);
+    OpColLct1<C> op1{static_cast<const C*>(in) + c0, static_cast<C*>(ws), ld, cw, W, (int)cw, R2, k, ptab,
+                     static_cast<const C*>(twr)};
+    if ((rc = tile<C, true, true, -1, OpColLct1<C>, W>(sh.l1, (long long)R2 * (cw / W), op1, st))) return rc;
+    OpColLct2<C> op2{static_cast<const C*>(ws), static_cast<C*>(out) + c0, ld, cw, W, (int)cw, R1, R2, k, cptab};
+    if ((rc = tile<C, true, true, -1, OpColLct2<C>, W>(sh.l2, (long long)R1 * (cw / W), op2, st))) return rc;
+  }
+  return XFT_OK;
 }
 
 }  // namespace

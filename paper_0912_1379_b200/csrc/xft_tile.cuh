@@ -17,6 +17,10 @@
 #pragma once
 #include "xft_pipe.cuh"
 
+#ifndef XFT_TILE_PREFETCH
+#define XFT_TILE_PREFETCH 0
+#endif
+
 namespace xftb {
 
 template <class C, int LOGL, int E, int W, bool LOAD_COL, bool STORE_COL, int SIGN, class Op>
@@ -33,10 +37,25 @@ xft_tile_kernel(long long ntiles, Op op, const C* __restrict__ tw) {
   const int w = LOAD_COL ? t % W : t / TR;
   const int j = LOAD_COL ? t / W : t % TR;
   auto noop = []() {};
+  C nxt[XFT_TILE_PREFETCH ? E : 1];
+  if constexpr (XFT_TILE_PREFETCH) {
+    if (blockIdx.x < ntiles)
+#pragma unroll
+      for (int s = 0; s < E; ++s) nxt[s] = op.load(blockIdx.x, w, j + s * TR);
+  }
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     C v[E];
+    if constexpr (XFT_TILE_PREFETCH) {
 #pragma unroll
-    for (int s = 0; s < E; ++s) v[s] = op.load(tile, w, j + s * TR);
+      for (int s = 0; s < E; ++s) v[s] = nxt[s];
+      // software pipelining: the next tile's loads are in flight during this tile's FFT and stores
+      if (tile + gridDim.x < ntiles)
+#pragma unroll
+        for (int s = 0; s < E; ++s) nxt[s] = op.load(tile + gridDim.x, w, j + s * TR);
+    } else {
+#pragma unroll
+      for (int s = 0; s < E; ++s) v[s] = op.load(tile, w, j + s * TR);
+    }
     pipe_passes<Fwd, 0>(v, smem + w * LS, j, tw, noop);
     if constexpr (Op::MID) {
 #pragma unroll
