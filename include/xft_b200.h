@@ -135,6 +135,22 @@ int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, i
 int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd_host,
                         int seg_log2w, int64_t seg_stride, void* stream);
 
+/* Composed transform in one launch (device in/out, parameters on the host):
+ * out = scale * R(L_{nst} ... L_2 L_1 in), 1 <= nst <= 4, each stage reading the
+ * previous stage's output as samples on the standard grid; R reverses the
+ * sample order when `reverse`.  The CLI inverse round trip of the reference
+ * (xft/cli.py:236-253) is nst = 2 with the scale-adjusted inverse, scale =
+ * sqrt(4b/pi), reverse = 1.  Power-of-two n, 32 <= n <= in-CTA limit. */
+int xft_lct_chain(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd_host, int nst,
+                  double scale, int reverse, void* stream);
+
+/* b = 0 branch (xft/lct.py:236-263), batched: out = sqrt(d) exp(i c d y^2/2) samples,
+ * y the grid nodes, samples = f(d y) supplied by the caller (device), abcd device
+ * (stride 0|4).  Host validation (b = 0, ad = 1, d > 0) in xft_validate_b_zero. */
+int xft_lct_b_zero(const void* samples, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+                   int64_t abcd_stride, void* stream);
+int xft_validate_b_zero(const double* abcd, int64_t count, int64_t stride, double tol, int64_t* bad_row);
+
 /* Tiled transpose used by the 2-D pass and the sharded all-to-all layout:
  * out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols. */
 int xft_transpose(const void* in, void* out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,

@@ -343,13 +343,10 @@ struct ThreadConst<Cfg, true> {
 // are taken once per tile, not per element)
 // ---------------------------------------------------------------------------
 template <class Cfg>
-__device__ __forceinline__ void pre_multiply(typename Cfg::C (&v)[Cfg::E], const typename Cfg::C* rs, int j,
-                                             const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
-                                             const RowConst& kc, const typename Cfg::C* __restrict__ ptab,
-                                             const void* tabv) {
+__device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], int j, const typename Cfg::Coef& rcs,
+                                          const ThreadConst<Cfg>& tc, const RowConst& kc,
+                                          const typename Cfg::C* __restrict__ ptab, const void* tabv) {
   constexpr int E = Cfg::E, TR = Cfg::TR;
-#pragma unroll
-  for (int s = 0; s < E; ++s) v[s] = rs[j + s * TR];
   if constexpr (Cfg::MODE == MODE_DFT) {
     return;
   } else {
@@ -396,6 +393,16 @@ __device__ __forceinline__ void pre_multiply(typename Cfg::C (&v)[Cfg::E], const
   }
 }
 
+template <class Cfg>
+__device__ __forceinline__ void pre_multiply(typename Cfg::C (&v)[Cfg::E], const typename Cfg::C* rs, int j,
+                                             const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
+                                             const RowConst& kc, const typename Cfg::C* __restrict__ ptab,
+                                             const void* tabv) {
+#pragma unroll
+  for (int s = 0; s < Cfg::E; ++s) v[s] = rs[j + s * Cfg::TR];
+  pre_apply<Cfg>(v, j, rcs, tc, kc, ptab, tabv);
+}
+
 // output addressing of one row: natural (seg_stride == 0) or split into
 // 2^segl-wide segments placed seg_stride apart (the all-to-all send layout of
 // the sharded 2-D transform: segment g of row r lands at g*seg_stride + r*2^segl)
@@ -410,25 +417,26 @@ struct OutRow {
   }
 };
 
-template <class Cfg>
-__device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const OutRow<typename Cfg::C>& dst, int j,
-                                           const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
-                                           const RowConst& kc, double2 cn, const typename Cfg::C* __restrict__ ptab,
-                                           const void* tabv) {
+// post-multiplier of element s of a thread's E registers, handed to emit(s, value)
+// (a streaming store in the row kernel, a register write-back in the chain kernel)
+template <class Cfg, class Emit>
+__device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, const typename Cfg::Coef& rcs,
+                                           const ThreadConst<Cfg>& tc, const RowConst& kc, double2 cn,
+                                           const typename Cfg::C* __restrict__ ptab, const void* tabv, Emit&& emit) {
   using C = typename Cfg::C;
   constexpr int E = Cfg::E, TR = Cfg::TR;
   if constexpr (Cfg::MODE == MODE_DFT) {
 #pragma unroll
-    for (int s = 0; s < E; ++s) st_stream(dst.at(j + s * TR), v[s]);
+    for (int s = 0; s < E; ++s) emit(s, v[s]);
   } else if constexpr (Cfg::MODE == MODE_SCALED) {
     const C c = to_c<C>(cn);
 #pragma unroll
-    for (int s = 0; s < E; ++s) st_stream(dst.at(j + s * TR), cmul(c, cmul(__ldg(&ptab[j + s * TR]), v[s])));
+    for (int s = 0; s < E; ++s) emit(s, cmul(c, cmul(__ldg(&ptab[j + s * TR]), v[s])));
   } else {
     if (rcs.post == 0) {
       const C g = rcs.g;
 #pragma unroll
-      for (int s = 0; s < E; ++s) st_stream(dst.at(j + s * TR), cmul(cmul(g, __ldg(&ptab[j + s * TR])), v[s]));
+      for (int s = 0; s < E; ++s) emit(s, cmul(cmul(g, __ldg(&ptab[j + s * TR])), v[s]));
       return;
     }
     if constexpr (!Cfg::C128) {
@@ -441,7 +449,7 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const O
         const int off = tc.off0 + 2 * s * TR;
         const uint32_t o2 = (uint32_t)(off * off);
         const uint32_t top = dhi * o2 + __umulhi(dlo, o2) + (b0 - (uint32_t)s * (1u << (31 - Cfg::LE)));
-        st_stream(dst.at(j + s * TR), cmul(unit_turns_sfu(top, g), v[s]));
+        emit(s, cmul(unit_turns_sfu(top, g), v[s]));
       }
     } else {
       const double2* tab = static_cast<const double2*>(tabv);
@@ -456,7 +464,7 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const O
           const double psi = __dmul_rn(cout, __dmul_rn(y, y));  // xft/kernel.py:113
           const double add = d0 - kStepPi16[s * (16 / E)];
           const double2 e = unit_phase_tab(psi, add, q0, tab);
-          st_stream(dst.at(j + s * TR), cmul(make_double2(e.x * g, e.y * g), v[s]));
+          emit(s, cmul(make_double2(e.x * g, e.y * g), v[s]));
         }
       } else {
 #pragma unroll
@@ -466,11 +474,20 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const O
           const double psi = __dmul_rn(cout, __dmul_rn(y, y));
           const double add = d0 - kStepPi16[s * (16 / E)];
           const double2 e = unit_phase_tab(prereduce(psi), add, q0, tab);
-          st_stream(dst.at(j + s * TR), cmul(make_double2(e.x * g, e.y * g), v[s]));
+          emit(s, cmul(make_double2(e.x * g, e.y * g), v[s]));
         }
       }
     }
   }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const OutRow<typename Cfg::C>& dst, int j,
+                                           const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
+                                           const RowConst& kc, double2 cn, const typename Cfg::C* __restrict__ ptab,
+                                           const void* tabv) {
+  post_apply<Cfg>(v, j, rcs, tc, kc, cn, ptab, tabv,
+                  [&](int s, typename Cfg::C o) { st_stream(dst.at(j + s * Cfg::TR), o); });
 }
 
 // ---------------------------------------------------------------------------

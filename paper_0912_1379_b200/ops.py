@@ -163,3 +163,60 @@ def lct_host(values: np.ndarray, abcd, *, bare_fourier=False, out=None,
     _native.call("xft_lct_host", v.ctypes.data, out.ctypes.data, v.shape[0], v.shape[1], code,
                  p.ctypes.data, 0 if p.shape[0] == 1 else 4, flags, int(bool(check_unimodular)), float(tol))
     return out
+
+
+def lct_chain_rows(values, stages, *, scale=1.0, reverse=False, out=None):
+    """L_k ... L_1 applied to every row in one launch (rows stay on chip between stages).
+
+    ``stages``: sequence of (a, b, c, d); each stage reads the previous output as
+    samples on the standard grid (xft/cli.py:236-253 semantics).
+    """
+    torch = _torch()
+    v = _rows_view(values)
+    B, n = v.shape
+    p = np.ascontiguousarray(np.asarray(stages, dtype=np.float64).reshape(-1, 4))
+    if out is None:
+        out = torch.empty_like(v)
+    with torch.cuda.device(v.device):
+        _native.call("xft_lct_chain", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v), p.ctypes.data,
+                     p.shape[0], float(scale), int(bool(reverse)), _stream_ptr(v.device))
+    return out
+
+
+def inverse_roundtrip_rows(values, abcd, *, out=None):
+    """Forward LCT then the scale-adjusted inverse (the reference CLI's --inverse, xft/cli.py:236-253).
+
+    Recovers the input samples up to the discretisation error, in one launch.
+    """
+    import math
+
+    a, b, c, d = (float(t) for t in np.asarray(abcd, dtype=np.float64).reshape(4))
+    if b <= 0:
+        raise ParameterError("--inverse requires b > 0")
+    sigma = 4.0 * b / math.pi
+    second = (d * sigma, -b / sigma, -c * sigma, a / sigma)
+    return lct_chain_rows(values, [(a, b, c, d), second], scale=math.sqrt(sigma), reverse=True, out=out)
+
+
+def lct_b_zero_rows(samples, abcd, *, out=None, tol=UNIMODULAR_TOL):
+    """b = 0 branch for a batch: sqrt(d) e^{i c d y^2/2} f(d y) (xft/lct.py:236-263).
+
+    ``samples``: [B, n] CUDA tensor of f(d y_j) values; ``abcd``: one quadruple or [B, 4].
+    """
+    torch = _torch()
+    v = _rows_view(samples)
+    B, n = v.shape
+    p_host = np.ascontiguousarray(np.asarray(abcd, dtype=np.float64).reshape(-1, 4))
+    bad = ctypes.c_int64(-1)
+    st = _native.lib().xft_validate_b_zero(p_host.ctypes.data, p_host.shape[0], 4 if p_host.shape[0] > 1 else 0,
+                                          float(tol), ctypes.byref(bad))
+    if st:
+        from .errors import raise_for
+        raise_for(st, f"b = 0 parameters (row {bad.value})")
+    p_dev = torch.from_numpy(p_host).to(v.device)
+    if out is None:
+        out = torch.empty_like(v)
+    with torch.cuda.device(v.device):
+        _native.call("xft_lct_b_zero", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v), p_dev.data_ptr(),
+                     0 if p_host.shape[0] == 1 else 4, _stream_ptr(v.device))
+    return out

@@ -64,6 +64,25 @@ def test_mehler_z_validation():
         assert lib.xft_validate_mehler_z(a.ctypes.data, 1, 2, ctypes.byref(bad)) == code, z
 
 
+def test_b_zero_validation_order():
+    """xft/lct.py:243-253: b != 0, then a*d = 1, then d > 0; per-row bad index."""
+    lib = _lib_or_skip()
+    bad = ctypes.c_int64(-1)
+
+    def v(P, stride=4):
+        P = np.ascontiguousarray(P, dtype=np.float64)
+        bad.value = -1
+        return lib.xft_validate_b_zero(P.ctypes.data, P.reshape(-1, 4).shape[0], stride, 1e-10, ctypes.byref(bad)), \
+            bad.value
+
+    assert v([[1.0, 0.0, 3.0, 1.0], [0.5, 0.0, 0.0, 2.0]]) == (0, -1)
+    assert v([[1.0, 0.0, 3.0, 1.0], [0.0, 1.0, -1.0, 0.0]]) == (2, 1)     # b != 0
+    assert v([[1.0, 0.0, 3.0, 1.0], [1.0, 0.0, 0.0, 2.0]]) == (2, 1)     # a d != 1
+    assert v([[-1.0, 0.0, 0.0, -1.0]]) == (5, 0)                         # d <= 0
+    assert v([[-1.0, 1.0, 0.0, -1.0]]) == (2, 0)                         # b checked first
+    assert v([[0.5, 0.0, 0.0, 2.0]], stride=0) == (0, -1)
+
+
 def test_status_mapping():
     with pytest.raises(errors.DegenerateParameterError):
         errors.raise_for(4, "x")
