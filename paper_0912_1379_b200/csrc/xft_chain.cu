@@ -38,7 +38,7 @@ xft_chain_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __rest
   extern __shared__ __align__(128) unsigned char xft_smem[];
   __shared__ Coef cs[4];
   C* xbuf = reinterpret_cast<C*>(xft_smem);
-  void* tab = xft_smem + size_t(Cfg::TILE) * sizeof(C);
+  void* tab = xft_smem + size_t(Cfg::STAGE) * sizeof(C);
   const int tid = threadIdx.x, lrow = tid / TR, j = tid - lrow * TR;
   const ThreadConst<Cfg> tc(j);
   if (tid < cp.nst) make_coef(cs[tid], nullptr, cp.st[tid], kc);
@@ -59,7 +59,7 @@ xft_chain_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __rest
     for (int k = 0; k < cp.nst; ++k) {
       const Coef rc = cs[k];
       pre_apply<Cfg>(v, j, rc, tc, kc, ptab, tab);
-      pipe_passes<Cfg, 0>(v, xbuf + lrow * N, j, tw, noop);
+      pipe_passes<Cfg, 0>(v, xbuf + lrow * Cfg::NP, j, tw, noop);
       post_apply<Cfg>(v, j, rc, tc, kc, cn, ptab, tab, [&](int s, C o) { v[s] = o; });
     }
     if (active) {

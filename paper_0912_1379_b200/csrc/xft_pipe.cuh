@@ -214,6 +214,44 @@ __device__ __forceinline__ float2 unit_turns_sfu(uint32_t t, float g) {
   return make_float2(c * g, s * g);
 }
 
+// e^{2 pi i t / 2^32} for a walk value t (TurnWalk below: the +512 rounding
+// and the -326 magic-constant correction are already folded in):
+// one LEA.HI, one FFMA, the SFU pair.  (12582912 + fm) c - K = fm c + 4.768e-7,
+// and 4.768e-7 rad = 325.95 units of 2^-32 turn.
+__device__ __forceinline__ float2 walk_phasor(uint32_t t) {
+  const float F = __int_as_float(0x4B400000 + ((int)t >> 10));  // 12582912 + fm, exact
+  const float th = fmaf(F, 1.4980281548560015e-06f, -18.84955596923828f);
+  float s, c;
+  __sincosf(th, &s, &c);
+  return make_float2(c, s);
+}
+
+// The c64 chirp phase of element s of a thread, in 2^-32 turns:
+//   t(s) = top32( dq * off_s^2 + lin0 - s * lstep )   (mod 2^64),  off_s = off0 + s * S2
+// is a quadratic in s: t(s+1) = t(s) + D(s), D(s+1) = D(s) + 2 dq S2^2, with D
+// carried in 64 bits (exact) and t in 32 (one dropped carry per step at most,
+// < 4e-9 turn over a row).  Replaces one 64x32 multiply per element with adds.
+struct TurnWalk {
+  uint32_t t;
+  unsigned long long d, dd;
+  __device__ __forceinline__ TurnWalk(unsigned long long dq, int off0, int S2, unsigned long long lin0,
+                                      unsigned long long lstep) {
+    const unsigned long long o0 = (unsigned long long)((long long)off0 * off0);
+    const unsigned long long b = (unsigned long long)(2ll * off0 * S2);
+    const unsigned long long c = (unsigned long long)((long long)S2 * S2);
+    const unsigned long long a = dq * o0 + lin0 + ((512ull - 326ull) << 32);
+    t = (uint32_t)(a >> 32);
+    d = dq * (b + c) - lstep;
+    dd = dq * (2 * c);
+  }
+  __device__ __forceinline__ uint32_t next() {
+    const uint32_t r = t;
+    t += (uint32_t)(d >> 32);
+    d += dd;
+    return r;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // configuration
 // ---------------------------------------------------------------------------
@@ -227,12 +265,17 @@ struct PipeCfg {
   static constexpr int THREADS_C = TR * ROWS;
   static constexpr int THREADS = THREADS_C;
   static constexpr int TILE = ROWS * N;
+  // exchange-buffer footprint of one row: one pad slot per 16 elements
+  // (pad_idx), so every Stockham store/load offset is a compile-time immediate
+  // and both sides stay bank-conflict free
+  static constexpr int NP = N + N / 16;
+  static constexpr int STAGE = ROWS * NP;  // a stage holds ROWS input rows (TMA, contiguous) / exchange rows
   static constexpr int LE = ilog2(E);
   static constexpr int NPASS = (LOG2N + LE - 1) / LE;
   static constexpr int R0 = 1 << (LOG2N - (NPASS - 1) * LE);
   static constexpr bool C128 = sizeof(C) == 16;
   static constexpr size_t TAB_BYTES = C128 ? XFT_C128_TABCOPIES * 256 * sizeof(double2) : 0;
-  static constexpr size_t SMEM = size_t(STAGES) * TILE * sizeof(C) + TAB_BYTES;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(C) + TAB_BYTES;
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
   static_assert(THREADS <= 1024, "threads");
@@ -243,9 +286,8 @@ struct PipeCfg {
   static constexpr int MINB = MINB_;
 };
 
-template <class C> struct SwzPeriod;
-template <> struct SwzPeriod<float2> { static constexpr int V = 256; };   // swz<float2> mixes bits 4..7
-template <> struct SwzPeriod<double2> { static constexpr int V = 128; };  // swz<double2> mixes bits 3..6
+// padded exchange index: element a of a row lives at a + a/16
+__device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 
 template <class Cfg, int P, class Release>
 __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
@@ -279,25 +321,23 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
   if constexpr (!LAST) {
     __syncthreads();  // every thread is done reading this buffer
     if constexpr (P == 0) release();  // (first-barrier hook)
+    // Stockham store: element t of butterfly i goes to base + t NS, base =
+    // (i - k) R + k.  (base mod 16) + (t NS mod 16) < 16 for every thread (NS
+    // and R are powers of two, k < NS), so pad_idx(base + t NS) =
+    // pad_idx(base) + t NS + (t NS) / 16: one address per butterfly.
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int i = j + b * TR;
       const int k = i & (NS - 1);
-      const int base = (i - k) * R + k;
+      C* dst = rs + pad_idx((i - k) * R + k);
 #pragma unroll
-      for (int t = 0; t < R; ++t) {
-        // the XOR swizzle only mixes bits below SWZ_PERIOD: strides that are
-        // multiples of it become plain immediate offsets
-        if constexpr (NS % SwzPeriod<C>::V == 0) rs[swz<C>(base) + t * NS] = v[b + t * NB];
-        else rs[swz<C>(base + t * NS)] = v[b + t * NB];
-      }
+      for (int t = 0; t < R; ++t) dst[t * NS + ((t * NS) >> 4)] = v[b + t * NB];
     }
     __syncthreads();
+    // j < TR and TR | 16 or 16 | TR: pad_idx(j + s TR) = pad_idx(j) + s TR + (s TR) / 16
+    const C* src = rs + pad_idx(j);
 #pragma unroll
-    for (int s = 0; s < E; ++s) {
-      if constexpr (TR % SwzPeriod<C>::V == 0) v[s] = rs[swz<C>(j) + s * TR];
-      else v[s] = rs[swz<C>(j + s * TR)];
-    }
+    for (int s = 0; s < E; ++s) v[s] = src[s * TR + ((s * TR) >> 4)];
   }
 }
 
@@ -359,15 +399,10 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], int j, c
     }
     if constexpr (Cfg::MODE == MODE_LCT) {
       if constexpr (!Cfg::C128) {
-        const float2* tab = static_cast<const float2*>(tabv);
-        const uint32_t dlo = (uint32_t)rcs.dq_in, dhi = (uint32_t)(rcs.dq_in >> 32);
+        // boundary phase (-1)^k e^{-i pi k/n} rides on the walk's linear term
+        TurnWalk w(rcs.dq_in, tc.off0, 2 * TR, (unsigned long long)tc.bt0 << 32, 1ull << (63 - Cfg::LE));
 #pragma unroll
-        for (int s = 0; s < E; ++s) {
-          const int off = tc.off0 + 2 * s * TR;
-          const uint32_t o2 = (uint32_t)(off * off);
-          const uint32_t top = dhi * o2 + __umulhi(dlo, o2) + (tc.bt0 - (uint32_t)s * (1u << (31 - Cfg::LE)));
-          v[s] = cmul(unit_turns_sfu(top, 1.0f), v[s]);
-        }
+        for (int s = 0; s < E; ++s) v[s] = cmul(walk_phasor(w.next()), v[s]);
       } else {
         const double2* tab = static_cast<const double2*>(tabv);
         const double cin = rcs.cin, half = kc.half;
@@ -440,17 +475,10 @@ __device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, 
       return;
     }
     if constexpr (!Cfg::C128) {
-      const float2* tab = static_cast<const float2*>(tabv);
-      const uint32_t dlo = (uint32_t)rcs.dq_out, dhi = (uint32_t)(rcs.dq_out >> 32);
-      const uint32_t b0 = tc.bt0 + rcs.gq;
-      const float g = rcs.gabs;
+      TurnWalk w(rcs.dq_out, tc.off0, 2 * TR, (unsigned long long)(tc.bt0 + rcs.gq) << 32, 1ull << (63 - Cfg::LE));
+      const float2 g = make_float2(rcs.gabs, rcs.gabs);
 #pragma unroll
-      for (int s = 0; s < E; ++s) {
-        const int off = tc.off0 + 2 * s * TR;
-        const uint32_t o2 = (uint32_t)(off * off);
-        const uint32_t top = dhi * o2 + __umulhi(dlo, o2) + (b0 - (uint32_t)s * (1u << (31 - Cfg::LE)));
-        emit(s, cmul(unit_turns_sfu(top, g), v[s]));
-      }
+      for (int s = 0; s < E; ++s) emit(s, cmul(walk_phasor(w.next()), p_mul(v[s], g)));
     } else {
       const double2* tab = static_cast<const double2*>(tabv);
       const double cout = rcs.cout, s4 = rcs.s4, half = kc.half, g = rcs.gabs;
@@ -486,8 +514,14 @@ __device__ __forceinline__ void post_store(typename Cfg::C (&v)[Cfg::E], const O
                                            const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
                                            const RowConst& kc, double2 cn, const typename Cfg::C* __restrict__ ptab,
                                            const void* tabv) {
-  post_apply<Cfg>(v, j, rcs, tc, kc, cn, ptab, tabv,
-                  [&](int s, typename Cfg::C o) { st_stream(dst.at(j + s * Cfg::TR), o); });
+  if (dst.seg_stride == 0) {  // row-uniform: one address per thread, immediate offsets
+    typename Cfg::C* p = dst.base + j;
+    post_apply<Cfg>(v, j, rcs, tc, kc, cn, ptab, tabv,
+                    [&](int s, typename Cfg::C o) { st_stream(p + s * Cfg::TR, o); });
+  } else {
+    post_apply<Cfg>(v, j, rcs, tc, kc, cn, ptab, tabv,
+                    [&](int s, typename Cfg::C o) { st_stream(dst.at(j + s * Cfg::TR), o); });
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -513,7 +547,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   __shared__ Coef coeft[CH][Cfg::MODE == MODE_LCT ? ROWS : 1];
 
   C* stage0 = reinterpret_cast<C*>(xft_smem);
-  void* tab = xft_smem + size_t(S) * Cfg::TILE * sizeof(C);
+  void* tab = xft_smem + size_t(S) * Cfg::STAGE * sizeof(C);
 
   const int tid = threadIdx.x;
   const int lrow = tid / Cfg::TR;
@@ -527,7 +561,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     const long long rows = batch - t * ROWS < ROWS ? batch - t * ROWS : ROWS;
     const uint32_t bytes = (uint32_t)(rows * N * sizeof(C));
     mbar_arrive_expect_tx(&bars[st], bytes);
-    tma_load_1d(stage0 + size_t(st) * Cfg::TILE, in + t * Cfg::TILE, bytes, &bars[st]);
+    tma_load_1d(stage0 + size_t(st) * Cfg::STAGE, in + t * Cfg::TILE, bytes, &bars[st]);
   };
   auto fill_coefs = [&](long long first_tile) {  // tiles first_tile + q*G, q < CH
     if constexpr (Cfg::MODE == MODE_LCT) {
@@ -566,7 +600,9 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
       }
     }
     mbar_wait(&bars[st], (uint32_t)((it / S) & 1));
-    C* rs = stage0 + size_t(st) * Cfg::TILE + size_t(lrow) * N;
+    C* const stg = stage0 + size_t(st) * Cfg::STAGE;
+    const C* rs = stg + size_t(lrow) * N;      // this row's input (TMA layout)
+    C* xs = stg + size_t(lrow) * Cfg::NP;      // this row's exchange buffer (read-after-barrier)
     Coef rc;
     if constexpr (Cfg::MODE == MODE_LCT) rc = coeft[it % CH][lrow];
 
@@ -589,7 +625,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
       __syncthreads();
       first_barrier();
     } else {
-      pipe_passes<Cfg, 0>(v, rs, j, tw, first_barrier);
+      pipe_passes<Cfg, 0>(v, xs, j, tw, first_barrier);
     }
     if constexpr (S == 1) {
       __syncthreads();

@@ -29,7 +29,7 @@ xft_tile_kernel(long long ntiles, Op op, const C* __restrict__ tw) {
   constexpr int L = 1 << LOGL, TR = L / E;
   using Fwd = PipeCfg<C, LOGL, E, MODE_DFT, SIGN, W, 1, 1>;
   using Inv = PipeCfg<C, LOGL, E, MODE_DFT, -SIGN, W, 1, 1>;
-  constexpr int LS = L + 1;  // padded line stride: adjacent lines start in different banks
+  constexpr int LS = Fwd::NP + 1;  // odd line stride: adjacent lines start in different banks
   extern __shared__ __align__(128) unsigned char xft_smem[];
   C* smem = reinterpret_cast<C*>(xft_smem);
   const int t = threadIdx.x;
@@ -80,7 +80,7 @@ xft_tile_kernel(long long ntiles, Op op, const C* __restrict__ tw) {
 
 template <class C, int LOGL, int W>
 constexpr size_t tile_smem() {
-  return size_t(W) * ((1 << LOGL) + 1) * sizeof(C);
+  return size_t(W) * ((1 << LOGL) + (1 << LOGL) / 16 + 1) * sizeof(C);
 }
 
 }  // namespace xftb
