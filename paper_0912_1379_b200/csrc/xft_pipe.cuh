@@ -59,11 +59,6 @@ static __constant__ double kC128Big[4] = {100.53096491487338, 3.91886975727153e-
                                    0.009947183943243459};
 
 // s * pi / 16, s = 0..15: the boundary-phase step between a thread's registers
-static __constant__ double kStepPi16[16] = {
-    0.0, 0.19634954084936207, 0.39269908169872414, 0.5890486225480862, 0.7853981633974483,
-    0.9817477042468103, 1.1780972450961724, 1.3744467859455345, 1.5707963267948966,
-    1.7671458676442586, 1.9634954084936207, 2.1598449493429825, 2.356194490192345,
-    2.552544031041707, 2.748893571891069, 2.945243112740431};
 
 // ---------------------------------------------------------------------------
 // per-row coefficients
@@ -369,13 +364,18 @@ struct ThreadConst<Cfg, false> {
 template <class Cfg>
 struct ThreadConst<Cfg, true> {
   double off0;  // 2j - n + 1
-  double d0;    // -pi j / n
-  int q0;       // (-1)^j in table units
+  // boundary phase (-1)^k e^{-i pi k/n}, k = j + s TR, in table units U = 2 pi/256:
+  // 128 (k & 1) - 128 k / n = [q0 - (128/E) s] + d0 / U, with the integer part
+  // going to the table index (q0, and a per-s immediate) and |d0| <= U/2
+  double d0;
+  int q0;
   __device__ __forceinline__ explicit ThreadConst(int j) {
     off0 = opaque((double)(2 * j - Cfg::N + 1));
-    d0 = opaque(-(XFT_PI / Cfg::N) * (double)j);
-    q0 = (j & 1) << 7;
+    const int jq = (128 * j + Cfg::N / 2) / Cfg::N;  // nearest integer to 128 j / n
+    d0 = opaque(-(double)(128 * j - jq * Cfg::N) * (6.283185307179586477 / (256.0 * Cfg::N)));
+    q0 = ((j & 1) << 7) - jq;
   }
+  static constexpr int qstep(int s) { return -(128 / Cfg::E) * s; }
 };
 
 // ---------------------------------------------------------------------------
@@ -411,16 +411,14 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], int j, c
           for (int s = 0; s < E; ++s) {
             const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);  // xft/hermite.py:87-89
             const double phi = __dmul_rn(cin, __dmul_rn(x, x));               // xft/kernel.py:102
-            const double add = tc.d0 - kStepPi16[s * (16 / E)];
-            v[s] = cmul(unit_phase_tab(phi, add, tc.q0, tab), v[s]);
+            v[s] = cmul(unit_phase_tab(phi, tc.d0, tc.q0 + tc.qstep(s), tab), v[s]);
           }
         } else {
 #pragma unroll
           for (int s = 0; s < E; ++s) {
             const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
             const double phi = __dmul_rn(cin, __dmul_rn(x, x));
-            const double add = tc.d0 - kStepPi16[s * (16 / E)];
-            v[s] = cmul(unit_phase_tab(prereduce(phi), add, tc.q0, tab), v[s]);
+            v[s] = cmul(unit_phase_tab(prereduce(phi), tc.d0, tc.q0 + tc.qstep(s), tab), v[s]);
           }
         }
       }
@@ -490,8 +488,7 @@ __device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, 
           const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
           const double y = __dmul_rn(s4, x);                    // xft/lct.py:196
           const double psi = __dmul_rn(cout, __dmul_rn(y, y));  // xft/kernel.py:113
-          const double add = d0 - kStepPi16[s * (16 / E)];
-          const double2 e = unit_phase_tab(psi, add, q0, tab);
+          const double2 e = unit_phase_tab(psi, d0, q0 + tc.qstep(s), tab);
           emit(s, cmul(make_double2(e.x * g, e.y * g), v[s]));
         }
       } else {
@@ -500,8 +497,7 @@ __device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, 
           const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
           const double y = __dmul_rn(s4, x);
           const double psi = __dmul_rn(cout, __dmul_rn(y, y));
-          const double add = d0 - kStepPi16[s * (16 / E)];
-          const double2 e = unit_phase_tab(prereduce(psi), add, q0, tab);
+          const double2 e = unit_phase_tab(prereduce(psi), d0, q0 + tc.qstep(s), tab);
           emit(s, cmul(make_double2(e.x * g, e.y * g), v[s]));
         }
       }
