@@ -45,7 +45,7 @@ xft_chain_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __rest
   if constexpr (Cfg::C128) {
     double2* t = static_cast<double2*>(tab);
     const double2* g = static_cast<const double2*>(gtab);
-    for (int m = tid; m < XFT_C128_TABCOPIES * 256; m += Cfg::THREADS) t[m] = g[XFT_C128_TABCOPIES == 8 ? m >> 3 : m];
+    for (int m = tid; m < C128_TABN; m += Cfg::THREADS) t[m] = g[m];
   }
   __syncthreads();
   auto noop = []() {};
@@ -58,7 +58,7 @@ xft_chain_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __rest
     for (int s = 0; s < E; ++s) v[s] = active ? in[row * N + j + s * TR] : czero<C>();
     for (int k = 0; k < cp.nst; ++k) {
       const Coef rc = cs[k];
-      pre_apply<Cfg>(v, j, rc, tc, kc, ptab, tab);
+      pre_apply<Cfg>(v, [&](int s) { return v[s]; }, j, rc, tc, kc, ptab, tab);
       pipe_passes<Cfg, 0>(v, xbuf + lrow * Cfg::NP, j, tw, noop);
       post_apply<Cfg>(v, j, rc, tc, kc, cn, ptab, tab, [&](int s, C o) { v[s] = o; });
     }

@@ -18,24 +18,25 @@
 //    e^{i(phi+delta)} = T[q mod 256] e^{i r}, q = rint((phi+delta)/(2pi/256)),
 //    r by a two-constant FMA Cody-Waite step (|r| <= pi/256), e^{ir} by a
 //    degree-6/7 Taylor polynomial (|err| < 1e-17), T a 256-entry table in
-//    shared memory.
+//    shared memory (XFT_C128_TABL; 1024/2048 entries with shorter
+//    polynomials measured slower).  The boundary phase's integer table steps
+//    ride on q; only a per-thread residual |delta| <= U/2 enters the fp64 math.
 //  * c64: the chirp phase in turns, frac(D k'^2 + boundary) with
 //    D = (a/2b) half^2 / 2pi, is evaluated exactly in 64-bit fixed point
-//    (integer multiply-high, wraps mod 1 turn), then MUFU sin/cos of the
-//    signed turn fraction.  No fp64 and no conversions per element.
+//    (wraps mod 1 turn).  Along a thread's elements the phase is a quadratic
+//    in s, so it is walked with integer adds (TurnWalk), then one LEA.HI +
+//    FFMA map the turn fraction to MUFU sin/cos.  No fp64 per element.
 // Twiddles come from a pass-major table (entry (t-1)*NS + k of pass p holds
 // w_{NS*E}^{t k}) so every warp's twiddle loads are coalesced.
 #pragma once
 #include <type_traits>
 
 #include "xft_rows.cuh"
+#include "xft_tables.h"
 #include "xft_tma.cuh"
 
 #ifndef XFT_SKELETON
 #define XFT_SKELETON 0  // tuning only: 1 = exchanges without math, 2 = pure copy
-#endif
-#ifndef XFT_C128_TABCOPIES
-#define XFT_C128_TABCOPIES 1
 #endif
 
 namespace xftb {
@@ -43,16 +44,18 @@ namespace xftb {
 #define XFT_PI 3.141592653589793116
 #define XFT_INV_2PI 0.15915494309189534561
 
-// fp64 constants live in the constant bank so DFMA/DMUL take them as c[] operands
+// fp64 constants live in the constant bank so DFMA/DMUL take them as c[] operands.
+// U = 2 pi / C128_TABN (the table step) in two parts, 1/U, and the Taylor
+// coefficients of sin / cos on |r| <= U/2 (the terms the table size needs).
 static __constant__ double kC128[8] = {
-    0.02454369260617026,      // 0 U_HI = 2 pi / 256
-    9.567553118338697e-19,    // 1 U_LO
-    40.74366543152521,        // 2 1/U
-    -1.6666666666666667e-01,  // 3 sin: -1/6
-    8.3333333333333333e-03,   // 4 sin:  1/120
-    -0.5,                     // 5 cos: -1/2
-    4.1666666666666667e-02,   // 6 cos:  1/24
-    -1.3888888888888889e-03,  // 7 cos: -1/720
+    6.283185307179586 / C128_TABN,                          // 0 U_HI
+    2.4492935982947064e-16 / C128_TABN,                     // 1 U_LO (2 pi - fl(2 pi)) / TABN
+    C128_TABN * 0.15915494309189535,                        // 2 1/U
+    -1.6666666666666667e-01,                                // 3 sin: -1/6
+    8.3333333333333333e-03,                                 // 4 sin:  1/120
+    -0.5,                                                   // 5 cos: -1/2
+    4.1666666666666667e-02,                                 // 6 cos:  1/24
+    -1.3888888888888889e-03,                                // 7 cos: -1/720
 };
 // 32 pi = 4096 U in three parts, and its inverse: pre-reduction for huge phases
 static __constant__ double kC128Big[4] = {100.53096491487338, 3.91886975727153e-15, -9.583263391098687e-32,
@@ -139,15 +142,16 @@ __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abc
   c.cin = __ddiv_rn(0.5 * a, b);      // (0.5j * a / b).imag     xft/kernel.py:102
   c.cout = __ddiv_rn(0.5 * d, b);     // (0.5j * d / b).imag     xft/kernel.py:113
   c.s4 = __ddiv_rn(4.0 * b, XFT_PI);  // 4.0 * b / np.pi        xft/lct.py:196
-  // arg G / U, U = 2pi/256: -64 red / n - 32 sgn(b) [+ 32]   (exact in fp64)
-  double v = -64.0 * (double)k.cnred / (double)(1ll << k.log2n) + ((b > 0.0) ? -32.0 : 32.0);
-  if (k.flags & FLAG_BARE_FOURIER) v += 32.0;
+  // arg G / U, U = 2pi/T: (T/256) (-64 red / n - 32 sgn(b) [+ 32])   (exact in fp64)
+  constexpr double Q = C128_TABN / 256.0;
+  double v = -64.0 * Q * (double)k.cnred / (double)(1ll << k.log2n) + ((b > 0.0) ? -32.0 * Q : 32.0 * Q);
+  if (k.flags & FLAG_BARE_FOURIER) v += 32.0 * Q;
   const double vi = rint(v);
   c.gi = (int)vi;
   c.gf = (v - vi) * kC128[0];
   c.gabs = g_abs(b, k);
   double s, co;
-  sincospi(v * (1.0 / 128.0), &s, &co);
+  sincospi(v * (2.0 / C128_TABN), &s, &co);
   c.g = make_double2(c.gabs * co, c.gabs * s);
   // largest |phase| on the row = |coef| x_max^2; the table reduction is exact
   // for |phi| < ~1e13, beyond 1e11 the row takes the full-range sincos path
@@ -162,7 +166,7 @@ __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abc
 // ---------------------------------------------------------------------------
 // unit phasors
 // ---------------------------------------------------------------------------
-// e^{i (phi + add)} e^{2 pi i qoff/256} in fp64 via the 256-entry table tab[m] = e^{2 pi i m/256}.
+// e^{i (phi + add)} e^{i U qoff} in fp64 via the table tab[m] = e^{i U m}, U = 2 pi / C128_TABN.
 // phi: exact fp64 chirp argument, |phi| < 1e12 (larger: prereduce first); |add| < 2 pi.
 __device__ __forceinline__ double2 unit_phase_tab(double phi, double add, int qoff, const double2* __restrict__ tab) {
   const double t = fma(phi + add, kC128[2], 6755399441055744.0);
@@ -172,11 +176,11 @@ __device__ __forceinline__ double2 unit_phase_tab(double phi, double add, int qo
   r = r + add;
   r = fma(-qd, kC128[1], r);
   const double z = r * r;
-  const double sn = fma(r * z, fma(z, kC128[4], kC128[3]), r);
-  const double cs = fma(z, fma(z, fma(z, kC128[7], kC128[6]), kC128[5]), 1.0);
-  // 8 interleaved copies: lane l reads copy (l & 7), so the 8 lanes of a
-  // 16-byte quarter-warp phase always hit 8 different bank groups
-  const double2 w = XFT_C128_TABCOPIES == 8 ? tab[((q & 255) << 3) | (threadIdx.x & 7)] : tab[q & 255];
+  // |r| <= pi / TABN: 256 -> sin to r^5, cos to r^6; 1024 -> cos to r^4; 2048 -> sin to r^3
+  const double sn = C128_TABN >= 2048 ? fma(r * z, kC128[3], r) : fma(r * z, fma(z, kC128[4], kC128[3]), r);
+  const double cs = C128_TABN >= 1024 ? fma(z, fma(z, kC128[6], kC128[5]), 1.0)
+                                      : fma(z, fma(z, fma(z, kC128[7], kC128[6]), kC128[5]), 1.0);
+  const double2 w = tab[q & (C128_TABN - 1)];
   return make_double2(w.x * cs - w.y * sn, w.x * sn + w.y * cs);
 }
 
@@ -269,7 +273,7 @@ struct PipeCfg {
   static constexpr int NPASS = (LOG2N + LE - 1) / LE;
   static constexpr int R0 = 1 << (LOG2N - (NPASS - 1) * LE);
   static constexpr bool C128 = sizeof(C) == 16;
-  static constexpr size_t TAB_BYTES = C128 ? XFT_C128_TABCOPIES * 256 * sizeof(double2) : 0;
+  static constexpr size_t TAB_BYTES = C128 ? C128_TABN * sizeof(double2) : 0;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(C) + TAB_BYTES;
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
@@ -364,37 +368,43 @@ struct ThreadConst<Cfg, false> {
 template <class Cfg>
 struct ThreadConst<Cfg, true> {
   double off0;  // 2j - n + 1
-  // boundary phase (-1)^k e^{-i pi k/n}, k = j + s TR, in table units U = 2 pi/256:
-  // 128 (k & 1) - 128 k / n = [q0 - (128/E) s] + d0 / U, with the integer part
-  // going to the table index (q0, and a per-s immediate) and |d0| <= U/2
+  // boundary phase (-1)^k e^{-i pi k/n}, k = j + s TR, in table units U = 2 pi/T
+  // (T = C128_TABN, H = T/2): H (k & 1) - H k / n = [q0 - (H/E) s] + d0 / U, the
+  // integer part going to the table index (q0, and a per-s immediate), |d0| <= U/2
+  static constexpr int H = C128_TABN / 2;
   double d0;
   int q0;
   __device__ __forceinline__ explicit ThreadConst(int j) {
     off0 = opaque((double)(2 * j - Cfg::N + 1));
-    const int jq = (128 * j + Cfg::N / 2) / Cfg::N;  // nearest integer to 128 j / n
-    d0 = opaque(-(double)(128 * j - jq * Cfg::N) * (6.283185307179586477 / (256.0 * Cfg::N)));
-    q0 = ((j & 1) << 7) - jq;
+    const int jq = (H * j + Cfg::N / 2) / Cfg::N;  // nearest integer to H j / n
+    d0 = opaque(-(double)(H * j - jq * Cfg::N) * (6.283185307179586477 / (double(C128_TABN) * Cfg::N)));
+    q0 = (j & 1) * H - jq;
   }
-  static constexpr int qstep(int s) { return -(128 / Cfg::E) * s; }
+  static constexpr int qstep(int s) { return -(H / Cfg::E) * s; }
 };
 
 // ---------------------------------------------------------------------------
 // pre / post multipliers over a thread's E registers (row-uniform branches
 // are taken once per tile, not per element)
 // ---------------------------------------------------------------------------
-template <class Cfg>
-__device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], int j, const typename Cfg::Coef& rcs,
-                                          const ThreadConst<Cfg>& tc, const RowConst& kc,
-                                          const typename Cfg::C* __restrict__ ptab, const void* tabv) {
+// v[s] = pre-multiplier(s) * ld(s): each element is fetched right where it is
+// used, so the phasor chains of later elements overlap earlier loads instead of
+// all E samples being held in registers before the first phasor starts
+template <class Cfg, class Load>
+__device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], Load&& ld, int j,
+                                          const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
+                                          const RowConst& kc, const typename Cfg::C* __restrict__ ptab,
+                                          const void* tabv) {
   constexpr int E = Cfg::E, TR = Cfg::TR;
   if constexpr (Cfg::MODE == MODE_DFT) {
-    return;
+#pragma unroll
+    for (int s = 0; s < E; ++s) v[s] = ld(s);
   } else {
     int mode = 0;
     if constexpr (Cfg::MODE == MODE_LCT) mode = rcs.pre;
     if (mode == 0) {
 #pragma unroll
-      for (int s = 0; s < E; ++s) v[s] = cmul(__ldg(&ptab[j + s * TR]), v[s]);
+      for (int s = 0; s < E; ++s) v[s] = cmul(__ldg(&ptab[j + s * TR]), ld(s));
       return;
     }
     if constexpr (Cfg::MODE == MODE_LCT) {
@@ -402,7 +412,7 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], int j, c
         // boundary phase (-1)^k e^{-i pi k/n} rides on the walk's linear term
         TurnWalk w(rcs.dq_in, tc.off0, 2 * TR, (unsigned long long)tc.bt0 << 32, 1ull << (63 - Cfg::LE));
 #pragma unroll
-        for (int s = 0; s < E; ++s) v[s] = cmul(walk_phasor(w.next()), v[s]);
+        for (int s = 0; s < E; ++s) v[s] = cmul(walk_phasor(w.next()), ld(s));
       } else {
         const double2* tab = static_cast<const double2*>(tabv);
         const double cin = rcs.cin, half = kc.half;
@@ -411,14 +421,14 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], int j, c
           for (int s = 0; s < E; ++s) {
             const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);  // xft/hermite.py:87-89
             const double phi = __dmul_rn(cin, __dmul_rn(x, x));               // xft/kernel.py:102
-            v[s] = cmul(unit_phase_tab(phi, tc.d0, tc.q0 + tc.qstep(s), tab), v[s]);
+            v[s] = cmul(unit_phase_tab(phi, tc.d0, tc.q0 + tc.qstep(s), tab), ld(s));
           }
         } else {
 #pragma unroll
           for (int s = 0; s < E; ++s) {
             const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
             const double phi = __dmul_rn(cin, __dmul_rn(x, x));
-            v[s] = cmul(unit_phase_tab(prereduce(phi), tc.d0, tc.q0 + tc.qstep(s), tab), v[s]);
+            v[s] = cmul(unit_phase_tab(prereduce(phi), tc.d0, tc.q0 + tc.qstep(s), tab), ld(s));
           }
         }
       }
@@ -431,9 +441,7 @@ __device__ __forceinline__ void pre_multiply(typename Cfg::C (&v)[Cfg::E], const
                                              const typename Cfg::Coef& rcs, const ThreadConst<Cfg>& tc,
                                              const RowConst& kc, const typename Cfg::C* __restrict__ ptab,
                                              const void* tabv) {
-#pragma unroll
-  for (int s = 0; s < Cfg::E; ++s) v[s] = rs[j + s * Cfg::TR];
-  pre_apply<Cfg>(v, j, rcs, tc, kc, ptab, tabv);
+  pre_apply<Cfg>(v, [&](int s) { return rs[j + s * Cfg::TR]; }, j, rcs, tc, kc, ptab, tabv);
 }
 
 // output addressing of one row: natural (seg_stride == 0) or split into
@@ -576,7 +584,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   if constexpr (Cfg::C128) {
     double2* t = static_cast<double2*>(tab);
     const double2* g = static_cast<const double2*>(gtab);
-    for (int m = tid; m < XFT_C128_TABCOPIES * 256; m += Cfg::THREADS) t[m] = g[XFT_C128_TABCOPIES == 8 ? m >> 3 : m];
+    for (int m = tid; m < C128_TABN; m += Cfg::THREADS) t[m] = g[m];
   }
   __syncthreads();
   long long tile = blockIdx.x;

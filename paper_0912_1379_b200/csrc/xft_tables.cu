@@ -109,8 +109,8 @@ int get_tables(int64_t n, int dtype, Tables* out, int radix) {
   }
   auto gt = g_gtab.find({dev, dtype});
   if (gt == g_gtab.end()) {
-    // chirp phasor tables: c128 e^{2 pi i m/256}, c64 e^{2 pi i m/1024}
-    const int tn = dtype == XFT_C64 ? 1024 : 256;
+    // chirp phasor tables: c128 e^{2 pi i m/C128_TABN}, c64 e^{2 pi i m/1024}
+    const int tn = dtype == XFT_C64 ? 1024 : C128_TABN;
     std::vector<double2> g(tn);
     std::vector<float2> gf(tn);
     for (int m = 0; m < tn; ++m) {

@@ -12,6 +12,11 @@ namespace xftb {
 #ifndef XFT_C128_E
 #define XFT_C128_E 16
 #endif
+// log2 of the c128 chirp phasor table size (tab[m] = e^{2 pi i m / 2^TABL})
+#ifndef XFT_C128_TABL
+#define XFT_C128_TABL 8
+#endif
+constexpr int C128_TABN = 1 << XFT_C128_TABL;
 constexpr int pipe_radix(int dtype, int l) {
   return dtype == 0 ? (l >= 14 ? 32 : 16) : (l >= 13 ? 16 : XFT_C128_E);
 }
@@ -19,7 +24,7 @@ constexpr int pipe_radix(int dtype, int l) {
 struct Tables {
   const void* tw = nullptr;    // pass-major twiddles of the pipelined kernel (see xft_pipe.cuh)
   const void* ptab = nullptr;  // n entries p_k = e^{i pi ((n-1)k mod 2n)/n}  (xft/kernel.py:51-65)
-  const void* gtab = nullptr;  // 256 entries e^{2 pi i m/256} (c128 chirp table)
+  const void* gtab = nullptr;  // C128_TABN entries e^{2 pi i m/C128_TABN} (c128 chirp table)
   double2 cn{0.0, 0.0};        // C(n)                                    (xft/kernel.py:45-48)
   double half = 0.0;           // (pi / sqrt(2n)) / 2                     (xft/hermite.py:74-89)
 };
