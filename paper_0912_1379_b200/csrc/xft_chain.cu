@@ -45,7 +45,8 @@ xft_chain_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __rest
   if constexpr (Cfg::C128) {
     double2* t = static_cast<double2*>(tab);
     const double2* g = static_cast<const double2*>(gtab);
-    for (int m = tid; m < C128_TABN; m += Cfg::THREADS) t[m] = g[m];
+    for (int m = tid; m < XFT_C128_TABCOPIES * C128_TABN; m += Cfg::THREADS)
+      t[m] = g[XFT_C128_TABCOPIES == 8 ? m >> 3 : m];
   }
   __syncthreads();
   auto noop = []() {};

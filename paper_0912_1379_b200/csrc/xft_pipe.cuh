@@ -33,6 +33,10 @@
 
 #include "xft_rows.cuh"
 #include "xft_tables.h"
+
+#ifndef XFT_C128_TABCOPIES
+#define XFT_C128_TABCOPIES 1
+#endif
 #include "xft_tma.cuh"
 
 #ifndef XFT_SKELETON
@@ -161,6 +165,10 @@ __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abc
   const double pmax_out = fabs(c.cout) * y2 * y2;
   c.pre = (a != 0.0) ? (pmax_in < 1e12 ? 1 : 2) : 0;
   c.post = (d != 0.0) ? (pmax_out < 1e12 ? 1 : 2) : 0;
+#ifdef XFT_NOCHIRP  // tuning only: time the kernel with the chirps replaced by the p_k table path
+  c.pre = (XFT_NOCHIRP & 1) ? 0 : c.pre;
+  c.post = (XFT_NOCHIRP & 2) ? 0 : c.post;
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -180,7 +188,10 @@ __device__ __forceinline__ double2 unit_phase_tab(double phi, double add, int qo
   const double sn = C128_TABN >= 2048 ? fma(r * z, kC128[3], r) : fma(r * z, fma(z, kC128[4], kC128[3]), r);
   const double cs = C128_TABN >= 1024 ? fma(z, fma(z, kC128[6], kC128[5]), 1.0)
                                       : fma(z, fma(z, fma(z, kC128[7], kC128[6]), kC128[5]), 1.0);
-  const double2 w = tab[q & (C128_TABN - 1)];
+  // XFT_C128_TABCOPIES = 8: lane l reads interleaved copy (l & 7), so the 8 lanes
+  // of a quarter-warp always hit 8 different 16-byte bank groups
+  const double2 w = XFT_C128_TABCOPIES == 8 ? tab[((q & (C128_TABN - 1)) << 3) | (threadIdx.x & 7)]
+                                            : tab[q & (C128_TABN - 1)];
   return make_double2(w.x * cs - w.y * sn, w.x * sn + w.y * cs);
 }
 
@@ -273,7 +284,7 @@ struct PipeCfg {
   static constexpr int NPASS = (LOG2N + LE - 1) / LE;
   static constexpr int R0 = 1 << (LOG2N - (NPASS - 1) * LE);
   static constexpr bool C128 = sizeof(C) == 16;
-  static constexpr size_t TAB_BYTES = C128 ? C128_TABN * sizeof(double2) : 0;
+  static constexpr size_t TAB_BYTES = C128 ? XFT_C128_TABCOPIES * C128_TABN * sizeof(double2) : 0;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(C) + TAB_BYTES;
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
@@ -288,9 +299,14 @@ struct PipeCfg {
 // padded exchange index: element a of a row lives at a + a/16
 __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 
-template <class Cfg, int P, class Release>
+// release(): runs right after the first exchange barrier (pass 0).
+// FREE_EARLY: after the last exchange's reads, one more barrier and free_hook()
+// -- the buffer is dead from there on, so a single-stage caller can start the
+// next tile's load under the last pass and the epilogue.
+template <class Cfg, int P, bool FREE_EARLY, class Release, class Free>
 __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
-                                          const typename Cfg::C* __restrict__ tw, Release&& release) {
+                                          const typename Cfg::C* __restrict__ tw, Release&& release,
+                                          Free&& free_hook) {
   using C = typename Cfg::C;
   constexpr int E = Cfg::E, TR = Cfg::TR;
   constexpr int R = (P == 0) ? Cfg::R0 : E;
@@ -337,16 +353,27 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     const C* src = rs + pad_idx(j);
 #pragma unroll
     for (int s = 0; s < E; ++s) v[s] = src[s * TR + ((s * TR) >> 4)];
+    if constexpr (FREE_EARLY && P == Cfg::NPASS - 2) {
+      __syncthreads();
+      free_hook();
+    }
+  }
+}
+
+template <class Cfg, int P, bool FREE_EARLY = false, class Release, class Free>
+__device__ __forceinline__ void pipe_passes(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
+                                            const typename Cfg::C* __restrict__ tw, Release&& release,
+                                            Free&& free_hook) {
+  if constexpr (P < Cfg::NPASS) {
+    pipe_pass<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook);
+    pipe_passes<Cfg, P + 1, FREE_EARLY>(v, rs, j, tw, release, free_hook);
   }
 }
 
 template <class Cfg, int P, class Release>
 __device__ __forceinline__ void pipe_passes(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
                                             const typename Cfg::C* __restrict__ tw, Release&& release) {
-  if constexpr (P < Cfg::NPASS) {
-    pipe_pass<Cfg, P>(v, rs, j, tw, release);
-    pipe_passes<Cfg, P + 1>(v, rs, j, tw, release);
-  }
+  pipe_passes<Cfg, P, false>(v, rs, j, tw, release, []() {});
 }
 
 // ---------------------------------------------------------------------------
@@ -584,7 +611,8 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   if constexpr (Cfg::C128) {
     double2* t = static_cast<double2*>(tab);
     const double2* g = static_cast<const double2*>(gtab);
-    for (int m = tid; m < C128_TABN; m += Cfg::THREADS) t[m] = g[m];
+    for (int m = tid; m < XFT_C128_TABCOPIES * C128_TABN; m += Cfg::THREADS)
+      t[m] = g[XFT_C128_TABCOPIES == 8 ? m >> 3 : m];
   }
   __syncthreads();
   long long tile = blockIdx.x;
@@ -625,15 +653,22 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
         if (nt < ntiles) issue(nt, (it + S - 1) % S);
       }
     };
+    // single stage: the next tile's load starts once the last exchange has been
+    // read (c64; for c128 the barrier in front of the fp64-heavy last pass
+    // costs more than the earlier load gains, measured 137 -> 146 us at cfg2)
+    constexpr bool EARLY = S == 1 && !Cfg::C128;
+    auto stage_free = [&]() {
+      if (tid == 0 && tile + G < ntiles) issue(tile + G, 0);
+    };
     if constexpr (XFT_SKELETON == 2) {
       __syncthreads();
       first_barrier();
     } else {
-      pipe_passes<Cfg, 0>(v, xs, j, tw, first_barrier);
+      pipe_passes<Cfg, 0, EARLY>(v, xs, j, tw, first_barrier, stage_free);
     }
-    if constexpr (S == 1) {
+    if constexpr (S == 1 && !EARLY) {
       __syncthreads();
-      if (tid == 0 && tile + G < ntiles) issue(tile + G, 0);
+      stage_free();
     }
 
     const long long row = tile * ROWS + lrow;
