@@ -97,6 +97,17 @@ int launch_pipe(const LaunchArgs& a) {
   if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
     return XFT_ECUDA;
+#ifdef XFT_CARVEOUT
+  {
+    // smallest shared-memory carveout that holds MINB CTAs: the rest of the
+    // 256 KB stays L1 for the (re-read every tile) twiddle table
+    const int pct = XFT_CARVEOUT > 0 ? XFT_CARVEOUT
+                                     : (int)((SH::MINB * (Cfg::SMEM + 4096) * 100 + 228 * 1024 - 1) / (228 * 1024));
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct) !=
+        cudaSuccess)
+      return XFT_ECUDA;
+  }
+#endif
   int& occ = occ_cache[dev & 63];
   if (occ == 0) {
     int o = 0, sms = 0;

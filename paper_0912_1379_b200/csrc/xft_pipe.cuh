@@ -34,6 +34,12 @@
 #include "xft_rows.cuh"
 #include "xft_tables.h"
 
+#ifndef XFT_NOMEM
+#define XFT_NOMEM 0  // tuning only: a CTA re-reads / rewrites its first tile (L2-resident: compute-bound timing)
+#endif
+#ifndef XFT_L2PF
+#define XFT_L2PF 0  // tiles of L2 bulk prefetch beyond the TMA ring (0 = off)
+#endif
 #ifndef XFT_C128_TABCOPIES
 #define XFT_C128_TABCOPIES 1
 #endif
@@ -320,7 +326,10 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     C u[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) u[t] = v[b + t * NB];
-    if constexpr (NS > 1 && XFT_SKELETON == 0) {
+#ifndef XFT_NOTW
+#define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
+#endif
+    if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW) {
       const C* twp = tw + Cfg::twoff(P) + k;
 #pragma unroll
       for (int t = 1; t < R; ++t) {
@@ -592,7 +601,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     const long long rows = batch - t * ROWS < ROWS ? batch - t * ROWS : ROWS;
     const uint32_t bytes = (uint32_t)(rows * N * sizeof(C));
     mbar_arrive_expect_tx(&bars[st], bytes);
-    tma_load_1d(stage0 + size_t(st) * Cfg::STAGE, in + t * Cfg::TILE, bytes, &bars[st]);
+    tma_load_1d(stage0 + size_t(st) * Cfg::STAGE, in + (XFT_NOMEM ? (long long)blockIdx.x : t) * Cfg::TILE, bytes, &bars[st]);
   };
   auto fill_coefs = [&](long long first_tile) {  // tiles first_tile + q*G, q < CH
     if constexpr (Cfg::MODE == MODE_LCT) {
@@ -632,6 +641,14 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
       }
     }
     mbar_wait(&bars[st], (uint32_t)((it / S) & 1));
+    if constexpr (XFT_L2PF > 0) {
+      // pull the tile XFT_L2PF ahead of the ring into L2 while this one is transformed
+      const long long pt = tile + (long long)(S - 1 + XFT_L2PF) * G;
+      if (tid == 0 && pt < ntiles) {
+        const long long rows = batch - pt * ROWS < ROWS ? batch - pt * ROWS : ROWS;
+        tma_prefetch_l2(in + pt * Cfg::TILE, (uint32_t)(rows * N * sizeof(C)));
+      }
+    }
     C* const stg = stage0 + size_t(st) * Cfg::STAGE;
     const C* rs = stg + size_t(lrow) * N;      // this row's input (TMA layout)
     C* xs = stg + size_t(lrow) * Cfg::NP;      // this row's exchange buffer (read-after-barrier)
@@ -678,7 +695,8 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
         for (int s = 0; s < Cfg::E; ++s) st_stream(out + row * N + j + s * Cfg::TR, v[s]);
     } else {
       if (row < batch) {
-        const OutRow<C> o{seg_stride ? out + (row << seg_log2w) : out + row * N, seg_stride, seg_log2w};
+        const OutRow<C> o{seg_stride ? out + (row << seg_log2w) : out + (XFT_NOMEM ? (long long)blockIdx.x * ROWS + lrow : row) * N, seg_stride,
+                          seg_log2w};
         post_store<Cfg>(v, o, j, rc, tc, kc, cn, ptab, tab);
       }
     }

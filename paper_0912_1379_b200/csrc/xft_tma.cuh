@@ -59,6 +59,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
       : "memory");
 }
 
+// global -> L2 bulk prefetch (no completion tracking): warms L2 for a later
+// tma_load_1d of the same bytes (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void tma_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
+
 // streaming store (evict-first): outputs are not re-read by this kernel
 __device__ __forceinline__ void st_stream(float2* p, float2 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
