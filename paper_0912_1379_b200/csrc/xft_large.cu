@@ -13,6 +13,9 @@
 // FFT, applies the conjugate twiddle, and an inverse column pass returns to
 // natural order fused with the post-multiplier.  Scratch lives in device
 // memory (L2-resident for the configurations of BASELINE.json).
+#include <cuda.h>  // CUtensorMap (the encoder is fetched with cudaGetDriverEntryPoint)
+#include <cudaTypedefs.h>
+
 #include <cmath>
 #include <complex>
 #include <map>
@@ -784,6 +787,273 @@ int lct_cols_narrow(const void* in, void* out, void* ws, int64_t R, int64_t ncol
   return tile<C, true, true, -1>(sh.l2, (long long)R1 * (ncols / W), op2, st);
 }
 
+// ---------------------------------------------------------------------------
+// Column LCT in ONE HBM round trip with a thread-block cluster (R = K * L).
+// The K CTAs of a cluster own W adjacent columns at a time (a "group"); CTA c
+// holds rows r = c + K m (m < L) of the group in shared memory:
+//   1. 3-D bulk-tensor TMA: box {W, 1, 256} over the view [R/K][K][ncols], so
+//      every row segment is W contiguous samples (64 B), double-buffered
+//      across groups;
+//   2. pre-chirp, length-L FFT down each column in registers + the padded
+//      exchange buffer (the row kernel's passes), twiddle w_R^{c k1};
+//   3. cluster barrier; CTA c' gathers Y_c[k1] for its k1 slice from all K
+//      CTAs through distributed shared memory, runs the length-K DFT across
+//      them (X[k1 + L k2] = sum_c w_K^{c k2} Y_c[k1]), post-chirps and stores
+//      row k1 + L k2 of the group: the natural-order output, 64-B segments.
+// Each sample crosses HBM once in, once out (the two-pass tile path reads and
+// writes it twice).  In place is safe: a group is fully read before any of it
+// is written, groups are disjoint.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t clu_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t clu_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t clu_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void clu_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t clu_map(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void clu_ld(uint32_t a, float2& v) {
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void clu_ld(uint32_t a, double2& v) {
+  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_addr(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void clu_sync_relaxed() {  // WAR only: the peers' DSMEM loads have been consumed
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+template <class C_, int K_, int LOGL_, int W_, int NBUF_, int MINB_>
+struct CluCfg {
+  using C = C_;
+  static constexpr int K = K_, LOGL = LOGL_, W = W_, NBUF = NBUF_, MINB = MINB_;
+  static constexpr int L = 1 << LOGL, E = 16, TR = L / E, THREADS = W * TR;
+  using Fft = PipeCfg<C, LOGL, E, MODE_DFT, -1, W, 1, 1>;
+  // line stride: a 128-byte wavefront covers S = 128/sizeof(C) lanes = W lines x S/W
+  // consecutive positions; LS = S/W (mod S) puts them in S distinct slots
+  static constexpr int S = 128 / (int)sizeof(C);
+  static constexpr int LS = Fft::NP + (((S / W) - Fft::NP % S) % S + S) % S;
+  static constexpr int BUF = ((W * LS > L * W ? W * LS : L * W) * (int)sizeof(C) + 127) / 128 * 128 / (int)sizeof(C);
+  static constexpr size_t SMEM = NBUF * size_t(BUF) * sizeof(C);
+  static constexpr int BOXM = L < 256 ? L : 256;
+  static constexpr int EW = (int)sizeof(C) / 8;  // 8-byte tensor elements per sample
+  static constexpr int PAIRS = (L / K) * W;      // (k1, column) pairs a CTA finishes per group
+  static_assert(THREADS <= 1024 && L % K == 0 && W <= S, "cluster column shape");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+xft_colclu_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __restrict__ out, long long ld,
+                  int ngroups, ColChirp ck, const double2* __restrict__ ptab, const double2* __restrict__ cptab,
+                  const typename Cfg::C* __restrict__ tw) {
+  using C = typename Cfg::C;
+  constexpr int K = Cfg::K, L = Cfg::L, W = Cfg::W, E = Cfg::E, TR = Cfg::TR, T = Cfg::THREADS, NB = Cfg::NBUF;
+  constexpr int LOGR = Cfg::LOGL + ilog2(K);
+  extern __shared__ __align__(128) unsigned char xft_smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  C* const buf0 = reinterpret_cast<C*>(xft_smem);
+  const int c = (int)clu_rank();
+  const int q = (int)clu_id(), nq = (int)clu_count();
+  const int t = threadIdx.x, w = t % W, j = t / W;
+  auto noop = []() {};
+  auto issue = [&](int g, int b) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[b], (uint32_t)(L * W * sizeof(C)));
+#pragma unroll 1
+    for (int m0 = 0; m0 < L; m0 += Cfg::BOXM)
+      tma_load_3d(buf0 + b * Cfg::BUF + m0 * W, &map, g * W * Cfg::EW, c, m0, &bars[b]);
+  };
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    if (q < ngroups) issue(q, 0);
+    if (NB == 2 && q + nq < ngroups) issue(q + nq, 1);
+  }
+  __syncthreads();
+  int it = 0;
+  for (int g = q; g < ngroups; g += nq, ++it) {
+    const int b = NB == 2 ? (it & 1) : 0;
+    C* const X = buf0 + b * Cfg::BUF;
+    mbar_wait(&bars[b], (uint32_t)((NB == 2 ? it >> 1 : it) & 1));
+    C v[E];
+    if constexpr (sizeof(C) == 8) {
+      // this thread's rows r = r0 + s K TR: the chirp + boundary phase is a quadratic walk in s
+      const int r0 = c + K * j;
+      const uint32_t bt0 = ((uint32_t)(r0 & 1) << 31) - ((uint32_t)r0 << (31 - LOGR));
+      TurnWalk wk(ck.dq_in, 2 * r0 - (1 << LOGR) + 1, 2 * K * TR, (unsigned long long)bt0 << 32,
+                  (unsigned long long)(K * TR) << (63 - LOGR));
+#pragma unroll
+      for (int s = 0; s < E; ++s) v[s] = cmul(walk_phasor(wk.next()), X[(j + s * TR) * W + w]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        const int m = j + s * TR;
+        v[s] = ColPhase<C>::pre(ck, ptab, c + (long long)K * m, X[m * W + w]);
+      }
+    }
+    pipe_passes<typename Cfg::Fft, 0>(v, X + w * Cfg::LS, j, tw, noop);
+    __syncthreads();  // the exchange buffer is dead; it now receives Y[k1][w]
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const int k1 = j + s * TR;
+      C y = v[s];
+      if constexpr (sizeof(C) == 8) {  // w_R^{c k1}, exact turns
+        y = cmul(walk_phasor((0u - ((uint32_t)(c * k1) << (32 - LOGR))) + ((512u - 326u) << 0)), y);
+      } else {
+        double sn, cs;
+        sincospi(-2.0 * (double)(c * k1) / (double)(K * L), &sn, &cs);
+        y = cmul(make_double2(cs, sn), y);
+      }
+      X[k1 * W + w] = y;
+    }
+    clu_sync();
+    const uint32_t xaddr = smem_addr(X);
+#pragma unroll 1
+    for (int p = t; p < Cfg::PAIRS; p += T) {
+      const int pw = p % W, k1 = c * (L / K) + p / W;
+      C y[K];
+      const uint32_t la = xaddr + (uint32_t)((k1 * W + pw) * sizeof(C));
+#pragma unroll
+      for (int cc = 0; cc < K; ++cc) clu_ld(clu_map(la, cc), y[cc]);
+      dft_r<K, -1>(y);
+      C* dst = out + (long long)k1 * ld + (long long)g * W + pw;
+      const long long step = (long long)L * ld;
+      if constexpr (sizeof(C) == 8) {
+        // output rows k1 + L k2: post-chirp + boundary + arg G walk in k2
+        const uint32_t bt0 = ((uint32_t)(k1 & 1) << 31) - ((uint32_t)k1 << (31 - LOGR)) + ck.gq;
+        TurnWalk wk(ck.dq_out, 2 * k1 - (1 << LOGR) + 1, 2 * L, (unsigned long long)bt0 << 32,
+                    (unsigned long long)L << (63 - LOGR));
+        const float2 gg = make_float2(ck.gabs, ck.gabs);
+#pragma unroll
+        for (int k2 = 0; k2 < K; ++k2) dst[k2 * step] = cmul(walk_phasor(wk.next()), p_mul(y[k2], gg));
+      } else {
+#pragma unroll
+        for (int k2 = 0; k2 < K; ++k2) dst[k2 * step] = ColPhase<C>::post(ck, cptab, k1 + (long long)L * k2, y[k2]);
+      }
+    }
+    clu_sync_relaxed();  // every peer is done reading this CTA's Y
+    if (t == 0) {
+      const int gn = g + NB * nq;
+      if (gn < ngroups) issue(gn, b);
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, []() {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+#ifndef XFT_CLU14
+#define XFT_CLU14 1  // R = 16384: 0 = 16-CTA clusters x 1024 rows, 1 = 8-CTA clusters x 2048 rows (half-width groups)
+#endif
+#ifndef XFT_COLCLU
+#define XFT_COLCLU 1  // 0: always use the two-pass tile path for tall columns
+#endif
+
+template <class C, int K, int LOGL, int W, int NBUF = 1, int MINB = 2>
+int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
+                  const double2* ptab, const double2* cptab, cudaStream_t st) {
+  using Cfg = CluCfg<C, K, LOGL, W, NBUF, MINB>;
+  constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
+  if (R != (int64_t)K * Cfg::L || ncols % W || ncols / W > INT32_MAX || ld % 2) return XFT_ENOTSUP;
+  auto enc = tensor_encoder();
+  if (!enc) return XFT_ENOTSUP;
+  Tables tb;
+  int rc = get_tables(Cfg::L, dtype, &tb, Cfg::E);
+  if (rc) return rc;
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {(cuuint64_t)(ncols * Cfg::EW), (cuuint64_t)K, (cuuint64_t)(R / K)};
+  const cuuint64_t strides[2] = {(cuuint64_t)(ld * sizeof(C)), (cuuint64_t)(K * ld * sizeof(C))};
+  const cuuint32_t box[3] = {(cuuint32_t)(W * Cfg::EW), 1u, (cuuint32_t)Cfg::BOXM};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(in), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return XFT_ENOTSUP;
+  auto kern = xft_colclu_kernel<Cfg>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
+    return XFT_ECUDA;
+  if (K > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return XFT_ENOTSUP;
+  }
+  const int groups = (int)(ncols / W);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = K;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(K * groups));
+  int maxc = 0;
+  if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) != cudaSuccess || maxc < 1) {
+    cudaGetLastError();
+    return XFT_ENOTSUP;
+  }
+  const int ncl = groups < maxc ? groups : maxc;
+  cfg.gridDim = dim3((unsigned)(K * ncl));
+  if (cudaLaunchKernelEx(&cfg, kern, map, static_cast<C*>(out), (long long)ld, groups, ck, ptab, cptab,
+                         static_cast<const C*>(tb.tw)) != cudaSuccess)
+    return XFT_ECUDA;
+  return XFT_OK;
+}
+
+// tall columns through the cluster kernel: R = K * 1024 (K = 2..16), 64-byte row segments
+template <class C>
+int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
+                     const double2* ptab, const double2* cptab, cudaStream_t st) {
+  constexpr int W = sizeof(C) == 8 ? 8 : 4;
+  if (!XFT_COLCLU || ncols % W) return XFT_ENOTSUP;
+  switch (log2_of(R)) {
+#if XFT_CLU14 == 1
+    case 14: return launch_colclu<C, 8, 11, W / 2>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+#else
+    case 14: return launch_colclu<C, 16, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+#endif
+    case 13: return launch_colclu<C, 8, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    case 12: return launch_colclu<C, 4, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    case 11: return launch_colclu<C, 2, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    default: return XFT_ENOTSUP;
+  }
+}
+
 #ifndef XFT_COLSLAB_MB
 #define XFT_COLSLAB_MB 4096  // L2-resident scratch per column slab (4096: one slab; smaller slabs measured slower)
 #endif
@@ -796,16 +1066,20 @@ int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int6
   constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
   constexpr int W = tile_w<C>() * XFT_COLW;
   const int l = log2_of(R);
+  if (l > LMAX) {  // tall columns: one HBM round trip through a cluster when the shape allows
+    const ColChirp k = col_chirp(abcd, R, bare);
+    const double2 *ptab = nullptr, *cptab = nullptr;
+    int rc = boundary_tables(R, &ptab, &cptab);
+    if (rc) return rc;
+    rc = lct_cols_cluster<C>(in, out, R, ncols, ld, k, ptab, cptab, st);
+    if (rc != XFT_ENOTSUP) return rc;
+  }
   // wide tiles for the two-pass (four-step) heights; one-pass heights use 128-byte tiles
   if (ncols % W || l <= LMAX) return lct_cols_narrow<C>(in, out, ws, R, ncols, ld, abcd, bare, st);
   const ColChirp k = col_chirp(abcd, R, bare);
   const double2 *ptab = nullptr, *cptab = nullptr;
   int rc = boundary_tables(R, &ptab, &cptab);
   if (rc) return rc;
-  if (l <= LMAX) {
-    OpColLctOne<C> op{static_cast<const C*>(in), static_cast<C*>(out), ld, W, k, ptab, cptab};
-    return tile<C, true, true, -1, OpColLctOne<C>, W>(l, ncols / W, op, st);
-  }
   const Shape sh = split(l);
   const int R1 = 1 << sh.l1, R2 = 1 << sh.l2;
   const void* twr = nullptr;

@@ -79,3 +79,32 @@ def test_config5_full(torch, L2):
     for c in (0, 777, n // 2, n - 1):
         _, ref = O.fast_lct_rows(ABCD5, rows_h[:, c].astype(complex))
         assert rel_l2(outh[:, c], ref) <= 2e-5
+
+
+@pytest.mark.parametrize("R", [2048, 4096, 8192, 16384])
+@pytest.mark.parametrize("dtype,tol", [(np.complex64, 2e-5), (np.complex128, 1e-12)])
+@pytest.mark.parametrize("inplace", [True, False])
+def test_columns_tall(torch, L2, R, dtype, tol, inplace):
+    """Tall column LCTs (the cluster path: K CTAs x 1024 rows share a column group through DSMEM).
+
+    Strided slab (row stride ld > n_cols), in place and out of place, against the
+    oracle's per-column fast_lct (xft/lct.py:168-208 down each column).
+    """
+    from paper_0912_1379_b200 import _native, ops
+
+    nc, ld = (24, 40) if dtype == np.complex64 else (12, 20)
+    rng = np.random.default_rng(R + nc)
+    full = (rng.normal(size=(R, ld)) + 1j * rng.normal(size=(R, ld))).astype(dtype)
+    src = torch.from_numpy(full).cuda()
+    dst = src if inplace else torch.zeros_like(src)
+    ws = torch.empty_like(src)
+    p = np.array((0.5, 1.5, -0.5, 0.5))
+    _native.call("xft_lct_columns", src.data_ptr(), dst.data_ptr(), R, nc, ld, ops._dtype_code(src), p.ctypes.data,
+                 ws.data_ptr(), ops._stream_ptr(src.device))
+    got = dst.cpu().numpy()
+    _, ref = O.fast_lct_rows(tuple(p), full[:, :nc].T.astype(complex))
+    assert rel_l2(got[:, :nc], ref.T) <= tol
+    if not inplace:
+        assert np.all(got[:, nc:] == 0)  # columns outside the slab untouched
+    else:
+        assert np.array_equal(got[:, nc:], full[:, nc:])
