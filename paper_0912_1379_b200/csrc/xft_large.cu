@@ -804,6 +804,25 @@ int lct_cols_narrow(const void* in, void* out, void* ws, int64_t R, int64_t ncol
 // writes it twice).  In place is safe: a group is fully read before any of it
 // is written, groups are disjoint.
 // ---------------------------------------------------------------------------
+#ifndef XFT_CLU14
+#define XFT_CLU14 1  // R = 16384: 0 = 16-CTA clusters x 1024 rows, 1 = 8-CTA clusters x 2048 rows (half-width groups)
+#endif
+#ifndef XFT_CLU_PROMO
+#define XFT_CLU_PROMO 0  // L2 promotion of the column-group TMA loads (bytes; 0 = none)
+#endif
+#ifndef XFT_CLU_PF
+#define XFT_CLU_PF 0  // L2 prefetch of the next group at the start of each group
+#endif
+#ifndef XFT_CLU_NB
+#define XFT_CLU_NB 1  // group buffers per CTA (2: double-buffered TMA)
+#endif
+#ifndef XFT_CLU_MINB
+#define XFT_CLU_MINB 2  // resident CTAs per SM the registers are sized for
+#endif
+#ifndef XFT_COLCLU
+#define XFT_COLCLU 1  // 0: always use the two-pass tile path for tall columns
+#endif
+
 __device__ __forceinline__ uint32_t clu_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -843,6 +862,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 
 __device__ __forceinline__ void clu_sync_relaxed() {  // WAR only: the peers' DSMEM loads have been consumed
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map), "r"(x), "r"(y), "r"(z)
+               : "memory");
 }
 
 template <class C_, int K_, int LOGL_, int W_, int NBUF_, int MINB_>
@@ -898,6 +922,12 @@ xft_colclu_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __re
     const int b = NB == 2 ? (it & 1) : 0;
     C* const X = buf0 + b * Cfg::BUF;
     mbar_wait(&bars[b], (uint32_t)((NB == 2 ? it >> 1 : it) & 1));
+    if (XFT_CLU_PF && t == 0 && g + NB * nq < ngroups) {
+      // warm L2 with the group this buffer takes next: its TMA load (issued after
+      // the gather) then streams from L2 instead of waiting on HBM
+#pragma unroll 1
+      for (int m0 = 0; m0 < L; m0 += Cfg::BOXM) tma_prefetch_3d(&map, (g + NB * nq) * W * Cfg::EW, c, m0);
+    }
     C v[E];
     if constexpr (sizeof(C) == 8) {
       // this thread's rows r = r0 + s K TR: the chirp + boundary phase is a quadratic walk in s
@@ -975,12 +1005,6 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
   return fn;
 }
 
-#ifndef XFT_CLU14
-#define XFT_CLU14 1  // R = 16384: 0 = 16-CTA clusters x 1024 rows, 1 = 8-CTA clusters x 2048 rows (half-width groups)
-#endif
-#ifndef XFT_COLCLU
-#define XFT_COLCLU 1  // 0: always use the two-pass tile path for tall columns
-#endif
 
 template <class C, int K, int LOGL, int W, int NBUF = 1, int MINB = 2>
 int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
@@ -999,7 +1023,10 @@ int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t l
   const cuuint32_t box[3] = {(cuuint32_t)(W * Cfg::EW), 1u, (cuuint32_t)Cfg::BOXM};
   const cuuint32_t estr[3] = {1u, 1u, 1u};
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(in), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          XFT_CLU_PROMO == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+          : XFT_CLU_PROMO == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+          : XFT_CLU_PROMO == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return XFT_ENOTSUP;
   auto kern = xft_colclu_kernel<Cfg>;
@@ -1043,9 +1070,9 @@ int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_
   if (!XFT_COLCLU || ncols % W) return XFT_ENOTSUP;
   switch (log2_of(R)) {
 #if XFT_CLU14 == 1
-    case 14: return launch_colclu<C, 8, 11, W / 2>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    case 14: return launch_colclu<C, 8, 11, W / 2, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st);
 #else
-    case 14: return launch_colclu<C, 16, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    case 14: return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st);
 #endif
     case 13: return launch_colclu<C, 8, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
     case 12: return launch_colclu<C, 4, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
