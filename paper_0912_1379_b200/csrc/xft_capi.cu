@@ -2,6 +2,8 @@
 // validation, the host end-to-end pipeline, the transpose and the 2-D pass.
 #include <array>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <utility>
 
@@ -228,6 +230,50 @@ int launch_transpose(const void* in, void* out, int64_t rows, int64_t cols, int6
 
 }  // namespace
 
+namespace {
+// persistent resources of the host-buffer path (xft_lct_host), one per device
+struct HostPipe {
+  static constexpr int NSLOT = 3;
+  std::mutex mu;
+  cudaStream_t st[NSLOT] = {};
+  void* buf[NSLOT][2] = {};
+  void* par[NSLOT] = {};
+  size_t cap = 0, pcap = 0;
+  int reserve(size_t bytes, size_t pbytes) {
+    for (int s = 0; s < NSLOT; ++s)
+      if (!st[s] && cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking) != cudaSuccess) return XFT_ECUDA;
+    if (bytes > cap) {
+      for (int s = 0; s < NSLOT; ++s) {
+        if (cudaStreamSynchronize(st[s]) != cudaSuccess) return XFT_ECUDA;
+        for (int h = 0; h < 2; ++h) {
+          if (buf[s][h]) cudaFree(buf[s][h]);
+          buf[s][h] = nullptr;
+          if (cudaMalloc(&buf[s][h], bytes) != cudaSuccess) return XFT_ECUDA;
+        }
+      }
+      cap = bytes;
+    }
+    if (pbytes > pcap) {
+      for (int s = 0; s < NSLOT; ++s) {
+        if (par[s]) cudaFree(par[s]);
+        par[s] = nullptr;
+        if (cudaMalloc(&par[s], pbytes) != cudaSuccess) return XFT_ECUDA;
+      }
+      pcap = pbytes;
+    }
+    return XFT_OK;
+  }
+};
+HostPipe& host_pipe(int dev) {
+  static std::mutex m;
+  static std::map<int, HostPipe*> pipes;
+  std::lock_guard<std::mutex> lock(m);
+  HostPipe*& p = pipes[dev];
+  if (!p) p = new HostPipe();
+  return *p;
+}
+}  // namespace
+
 extern "C" {
 
 int xft_version(void) { return 100; }
@@ -353,50 +399,41 @@ int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype,
   int64_t chunk = (int64_t)((16u << 20) / row_bytes);
   if (chunk < 1) chunk = 1;
   if (chunk > batch) chunk = batch;
-  constexpr int NSLOT = 3;
-  cudaStream_t st[NSLOT] = {};
-  void* dbuf[NSLOT][2] = {};
-  double* dpar[NSLOT] = {};
-  rc = XFT_OK;
-  for (int s = 0; s < NSLOT && !rc; ++s) {
-    if (cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking) != cudaSuccess) rc = XFT_ECUDA;
-    else if (cudaMallocAsync(&dbuf[s][0], row_bytes * chunk, st[s]) != cudaSuccess) rc = XFT_ECUDA;
-    else if (cudaMallocAsync(&dbuf[s][1], row_bytes * chunk, st[s]) != cudaSuccess) rc = XFT_ECUDA;
-    else if (abcd_stride && cudaMallocAsync((void**)&dpar[s], sizeof(double) * abcd_stride * chunk, st[s]) != cudaSuccess)
-      rc = XFT_ECUDA;
-  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
+  // per-device persistent streams and staging buffers (grown on demand, never
+  // freed): no allocation, stream creation or pool trimming inside the call
+  HostPipe& hp = host_pipe(dev);
+  std::lock_guard<std::mutex> lock(hp.mu);
+  rc = hp.reserve(row_bytes * (size_t)chunk, abcd_stride ? sizeof(double) * abcd_stride * (size_t)chunk : 0);
+  if (rc) return rc;
   const Abcd uni = abcd_stride ? Abcd{0, 0, 0, 0} : Abcd{abcd[0], abcd[1], abcd[2], abcd[3]};
   for (int64_t r0 = 0, c = 0; r0 < batch && !rc; r0 += chunk, ++c) {
-    const int s = (int)(c % NSLOT);
+    const int s = (int)(c % HostPipe::NSLOT);
     const int64_t rows = (batch - r0 < chunk) ? batch - r0 : chunk;
     const char* hin = static_cast<const char*>(in) + row_bytes * r0;
     char* hout = static_cast<char*>(out) + row_bytes * r0;
-    if (cudaMemcpyAsync(dbuf[s][0], hin, row_bytes * rows, cudaMemcpyHostToDevice, st[s]) != cudaSuccess) {
+    cudaStream_t st = hp.st[s];
+    if (cudaMemcpyAsync(hp.buf[s][0], hin, row_bytes * rows, cudaMemcpyHostToDevice, st) != cudaSuccess) {
       rc = XFT_ECUDA;
       break;
     }
     const double* dp = nullptr;
     if (abcd_stride) {
-      if (cudaMemcpyAsync(dpar[s], abcd + abcd_stride * r0, sizeof(double) * abcd_stride * rows,
-                          cudaMemcpyHostToDevice, st[s]) != cudaSuccess) {
+      if (cudaMemcpyAsync(hp.par[s], abcd + abcd_stride * r0, sizeof(double) * abcd_stride * rows,
+                          cudaMemcpyHostToDevice, st) != cudaSuccess) {
         rc = XFT_ECUDA;
         break;
       }
-      dp = dpar[s];
+      dp = static_cast<const double*>(hp.par[s]);
     }
-    rc = run_rows(MODE_LCT, -1, dbuf[s][0], dbuf[s][1], rows, n, dtype, dp, abcd_stride, uni, flags, st[s]);
+    rc = run_rows(MODE_LCT, -1, hp.buf[s][0], hp.buf[s][1], rows, n, dtype, dp, abcd_stride, uni, flags, st);
     if (rc) break;
-    if (cudaMemcpyAsync(hout, dbuf[s][1], row_bytes * rows, cudaMemcpyDeviceToHost, st[s]) != cudaSuccess)
+    if (cudaMemcpyAsync(hout, hp.buf[s][1], row_bytes * rows, cudaMemcpyDeviceToHost, st) != cudaSuccess)
       rc = XFT_ECUDA;
   }
-  for (int s = 0; s < NSLOT; ++s) {
-    if (!st[s]) continue;
-    if (dbuf[s][0]) cudaFreeAsync(dbuf[s][0], st[s]);
-    if (dbuf[s][1]) cudaFreeAsync(dbuf[s][1], st[s]);
-    if (dpar[s]) cudaFreeAsync(dpar[s], st[s]);
-    if (cudaStreamSynchronize(st[s]) != cudaSuccess && !rc) rc = XFT_ECUDA;
-    cudaStreamDestroy(st[s]);
-  }
+  for (int s = 0; s < HostPipe::NSLOT; ++s)
+    if (cudaStreamSynchronize(hp.st[s]) != cudaSuccess && !rc) rc = XFT_ECUDA;
   return rc;
 }
 
