@@ -4,6 +4,7 @@
 // dtype, mode) on the host in long double and cached (immutable).
 #include <array>
 #include <cmath>
+#include <cstring>
 #include <complex>
 #include <map>
 #include <mutex>
@@ -236,6 +237,75 @@ MehlerPlanRow mehler_row(std::complex<double> z, int64_t n) {
 
 }  // namespace
 
+// A Mehler "plan": the per-row parameters, size classes and row lists of one
+// z array (the B200 analogue of frft_matrix_asymptotic's DenseTransform,
+// xft/dense.py:139-151), built on the host once and kept on the device.  Calls
+// with the same (n, z) reuse it: no host work, no copies, no synchronisation.
+struct MehlerPlan {
+  OpMehlerRow* rows = nullptr;              // [batch] device
+  int* list = nullptr;                      // [batch] device, rows grouped by class
+  std::vector<std::pair<int, long long>> classes;  // (log2 M, count) in list order
+  int maxl = 0;
+};
+
+int mehler_plan(int dev, int64_t batch, int64_t n, const double* z, int64_t z_stride, const MehlerPlan** out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int64_t, int64_t, uint64_t>, MehlerPlan> cache;
+  static std::vector<std::tuple<int, int64_t, int64_t, uint64_t>> order;  // insertion order (bounded cache)
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the z values as used
+  for (int64_t r = 0; r < batch; ++r) {
+    const double* zz = z + (z_stride ? r * z_stride : 0);
+    uint64_t bits[2];
+    std::memcpy(bits, zz, sizeof(bits));
+    for (int w = 0; w < 2; ++w)
+      for (int b = 0; b < 8; ++b) h = (h ^ ((bits[w] >> (8 * b)) & 0xff)) * 1099511628211ull;
+  }
+  const auto key = std::make_tuple(dev, batch, n, h);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = &it->second;
+    return XFT_OK;
+  }
+  std::vector<OpMehlerRow> rows(batch);
+  std::map<int, std::vector<int>> classes;
+  for (int64_t r = 0; r < batch; ++r) {
+    const double* zz = z + (z_stride ? r * z_stride : 0);
+    const MehlerPlanRow pr = mehler_row(std::complex<double>(zz[0], zz[1]), n);
+    rows[r] = pr.p;
+    classes[pr.l].push_back((int)r);
+  }
+  MehlerPlan p;
+  std::vector<int> list;
+  list.reserve(batch);
+  for (auto& kv : classes) {
+    list.insert(list.end(), kv.second.begin(), kv.second.end());
+    p.classes.emplace_back(kv.first, (long long)kv.second.size());
+    if (kv.first <= MAXL_C128) p.maxl = kv.first;
+  }
+  if (cudaMalloc(&p.rows, batch * sizeof(OpMehlerRow)) != cudaSuccess ||
+      cudaMalloc(&p.list, batch * sizeof(int)) != cudaSuccess ||
+      cudaMemcpy(p.rows, rows.data(), batch * sizeof(OpMehlerRow), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(p.list, list.data(), batch * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(p.rows);
+    cudaFree(p.list);
+    return XFT_ECUDA;
+  }
+  if (order.size() >= 8) {  // bounded: drop the oldest plan (callers are stream-ordered behind us)
+    auto old = cache.find(order.front());
+    if (old != cache.end()) {
+      cudaDeviceSynchronize();
+      cudaFree(old->second.rows);
+      cudaFree(old->second.list);
+      cache.erase(old);
+    }
+    order.erase(order.begin());
+  }
+  order.push_back(key);
+  *out = &cache.emplace(key, std::move(p)).first->second;
+  return XFT_OK;
+}
+
 extern "C" {
 
 int64_t xft_mehler_workspace_bytes(int64_t batch, int64_t n) {
@@ -252,59 +322,29 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
   if (rc) return rc;
   if (batch == 0) return XFT_OK;
   auto st = static_cast<cudaStream_t>(stream);
-  // per-row parameters and size classes
-  std::vector<MehlerPlanRow> pr(batch);
-  std::map<int, std::vector<int>> classes;
-  for (int64_t r = 0; r < batch; ++r) {
-    const double* zz = z + (z_stride ? r * z_stride : 0);
-    pr[r] = mehler_row(std::complex<double>(zz[0], zz[1]), n);
-    classes[pr[r].l].push_back((int)r);
-  }
-  std::vector<OpMehlerRow> rows(batch);
-  for (int64_t r = 0; r < batch; ++r) rows[r] = pr[r].p;
-  std::vector<int> order;
-  order.reserve(batch);
-  for (auto& kv : classes) order.insert(order.end(), kv.second.begin(), kv.second.end());
-  // device scratch: row table, row lists, one kernel-spectrum row per launched CTA
-  int maxl = 0;  // largest class served by the in-CTA kernel (scratch sizing)
-  for (auto& kv : classes)
-    if (kv.first <= MAXL_C128) maxl = kv.first;
-  const size_t tab_bytes = (size_t)batch * sizeof(OpMehlerRow);
-  const size_t list_bytes = ((size_t)batch * sizeof(int) + 255) & ~size_t(255);
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << maxl) * sizeof(double2);
-  char* ws = static_cast<char*>(workspace);
-  bool own = false;
-  const size_t need = ((tab_bytes + 255) & ~size_t(255)) + list_bytes + hs_bytes;
-  if (!ws) {
-    if (cudaMallocAsync((void**)&ws, need, st) != cudaSuccess) return XFT_ECUDA;
-    own = true;
-  }
-  OpMehlerRow* d_rows = reinterpret_cast<OpMehlerRow*>(ws);
-  int* d_list = reinterpret_cast<int*>(ws + ((tab_bytes + 255) & ~size_t(255)));
-  double2* d_hs = reinterpret_cast<double2*>(ws + ((tab_bytes + 255) & ~size_t(255)) + list_bytes);
-  if (cudaMemcpyAsync(d_rows, rows.data(), tab_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaMemcpyAsync(d_list, order.data(), batch * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess) {
-    if (own) cudaFreeAsync(ws, st);
-    return XFT_ECUDA;
-  }
+  const MehlerPlan* plan = nullptr;
+  if ((rc = mehler_plan(dev, batch, n, z, z_stride, &plan))) return rc;
+  // per launched CTA one kernel-spectrum row of the largest in-CTA class
+  const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << plan->maxl) * sizeof(double2);
+  double2* d_hs = static_cast<double2*>(workspace);
+  if (!d_hs && cudaMallocAsync((void**)&d_hs, hs_bytes, st) != cudaSuccess) return XFT_ECUDA;
   OpMehler op;
-  op.rows = d_rows;
+  op.rows = plan->rows;
   op.hscratch = d_hs;
   op.half = host_half_step(n);
   op.n = (int)n;
   size_t off = 0;
-  for (auto& kv : classes) {
-    const long long cnt = (long long)kv.second.size();
-    rc = kv.first <= MAXL_C128 ? blue<double2>(kv.first, in, out, cnt, d_list + off, op, st)
-                               : run_large_mehler(in, out, cnt, d_list + off, d_rows, kv.first, n, st);
+  for (const auto& cl : plan->classes) {
+    const long long cnt = cl.second;
+    rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan->list + off, op, st)
+                               : run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, st);
     if (rc) break;
     off += cnt;
   }
-  if (own) cudaFreeAsync(ws, st);
-  // (the pageable host vectors above were staged by cudaMemcpyAsync before it returned)
+  if (!workspace) cudaFreeAsync(d_hs, st);
   return rc;
 }
 

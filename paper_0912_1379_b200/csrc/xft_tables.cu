@@ -77,6 +77,17 @@ int get_tables(int64_t n, int dtype, Tables* out, int radix) {
   out->cn = host_kernel_prefactor(n);
   out->half = host_half_step(n);
   std::lock_guard<std::mutex> lk(g_mu);
+  static std::map<int, bool> pool_kept;
+  if (!pool_kept[dev]) {
+    // stream-ordered scratch of the large-row / Mehler / 2-D paths comes from the
+    // default pool: keep freed blocks cached instead of unmapping them at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_kept[dev] = true;
+  }
   int l = 0;
   while ((int64_t(1) << l) < n) ++l;
   const int E = radix > 0 ? radix : pipe_radix(dtype, l);
