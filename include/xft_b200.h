@@ -151,6 +151,23 @@ int xft_lct_b_zero(const void* samples, void* out, int64_t batch, int64_t n, int
                    int64_t abcd_stride, void* stream);
 int xft_validate_b_zero(const double* abcd, int64_t count, int64_t stride, double tol, int64_t* bad_row);
 
+/* ---- dense O(n^2) oracles on the GPU, complex128 only ----
+ * Independent, entry-by-entry evaluations of the reference's dense matrices
+ * (no FFT): applied matrix-free to [batch][n] vectors (any n), or materialised
+ * as [n][n] row-major (n <= 4096, xft/dense.py:44 MAX_DENSE_N). */
+/* out = L in, L = dense_lct_matrix(n, abcd) (xft/dense.py:230-249); abcd == NULL: the
+ * scaled Fourier matrix F (xft/kernel.py:68-80).  abcd on the host. */
+int xft_dense_lct_apply(const void* in, void* out, int64_t batch, int64_t n, const double* abcd_host, void* stream);
+/* out = (K_z(x_j, x_k) dx) in, frft_matrix_asymptotic (xft/dense.py:122-151); z host (stride 0|2). */
+int xft_dense_mehler_apply(const void* in, void* out, int64_t batch, int64_t n, const double* z_host,
+                           int64_t z_stride, void* stream);
+/* [n][n] entries: kind 0 = F, 1 = L (param = abcd), 2 = Mehler (param = z re, im). */
+int xft_dense_entries(void* out, int64_t n, int kind, const double* param_host, void* stream);
+/* Trapezoid sums of the quadrature oracle (xft/oracle.py:127-169), device buffers:
+ * out[j] = sum_p exp(-i (y_j x_p) / b) base[p]   (x, ys fp64; base, out complex128). */
+int xft_quadrature_sum(const double* x, const void* base, int64_t P, const double* ys, int64_t ny, double b,
+                       void* out, void* stream);
+
 /* Tiled transpose used by the 2-D pass and the sharded all-to-all layout:
  * out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols. */
 int xft_transpose(const void* in, void* out, int64_t rows, int64_t cols, int64_t ld_in, int64_t ld_out,

@@ -5,7 +5,8 @@ g_j = sum_k K_z(x_j, x_k) dx f_k on the asymptotic grid, with
 K_z(x,y) = sqrt(2/(1-z^2)) exp(-((1+z^2)(x^2+y^2) - 4xyz) / (2(1-z^2)))
 (xft/dense.py:122-136).  The reference materialises the n x n matrix (n <= 4096);
 here ``apply`` runs the O(n log n) windowed Bluestein kernel of libxft_b200.so
-for any n, and the dense ``entries`` are only built on request (n <= 4096).
+for any n, and the dense ``entries`` are only built on request (n <= 4096, on
+the GPU, entry by entry -- see dense.py).
 """
 from __future__ import annotations
 
@@ -81,31 +82,53 @@ def mehler_rows(values, z, *, out=None):
 
 @dataclass(frozen=True)
 class DenseTransform:
-    """Drop-in for the reference's DenseTransform (xft/dense.py:62-80) of the Mehler path.
+    """Drop-in for the reference's DenseTransform (xft/dense.py:62-80).
 
-    ``apply`` evaluates the transform with the fast GPU kernel; ``entries`` (the
-    dense matrix) is materialised lazily and only for n <= 4096.
+    provenance "chirp_factored" (frft_matrix_asymptotic, detail = z) or "lct"
+    (dense_lct_matrix, detail = (a, b, c, d)).  ``entries`` are built on the GPU
+    entry by entry (n <= 4096); ``apply`` runs the fast kernel for the Mehler
+    case and the matrix-free dense product for "lct"; ``apply_dense`` is always
+    the O(n^2) entry-by-entry product (any n) -- the independent check.
     """
 
     n: int
     provenance: str
     detail: object = field(default=None)
 
+    def _kind(self):
+        from . import dense
+
+        return dense.KIND_MEHLER if self.provenance == "chirp_factored" else dense.KIND_LCT
+
     @property
     def entries(self) -> np.ndarray:
+        from . import dense
+
         if self.n > MAX_DENSE_N:
             raise InvalidSizeError(f"dense path materializes only n <= {MAX_DENSE_N} (got {self.n})")
-        grid = asymptotic_zeros(self.n)
-        x = grid.nodes
-        return mehler_kernel(FrftOrder(self.detail), x[:, None], x[None, :]) * grid.spacing
+        return dense.dense_entries(self.n, self._kind(), self.detail).cpu().numpy()
 
-    def apply(self, v) -> np.ndarray:
+    def _vector(self, v):
         v = np.asarray(v, dtype=complex)
         if v.shape != (self.n,):
             raise ShapeError(f"expected a vector of length {self.n}, got {v.shape}")
+        return v
+
+    def apply(self, v) -> np.ndarray:
+        v = self._vector(v)
+        if self.provenance != "chirp_factored":
+            return self.apply_dense(v)
         torch = ops._torch()
         t = torch.from_numpy(v).to("cuda")
         return mehler_rows(t, self.detail)[0].cpu().numpy()
+
+    def apply_dense(self, v) -> np.ndarray:
+        from . import dense
+
+        v = self._vector(v)
+        if self.provenance == "chirp_factored":
+            return dense.dense_mehler_apply(v, self.detail)[0].cpu().numpy()
+        return dense.dense_lct_apply(v, self.detail)[0].cpu().numpy()
 
 
 def frft_matrix_asymptotic(n: int, order: FrftOrder) -> DenseTransform:
