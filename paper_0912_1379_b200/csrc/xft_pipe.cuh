@@ -309,10 +309,13 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 // FREE_EARLY: after the last exchange's reads, one more barrier and free_hook()
 // -- the buffer is dead from there on, so a single-stage caller can start the
 // next tile's load under the last pass and the epilogue.
+#ifndef XFT_TWPRE
+#define XFT_TWPRE 0  // 1: load the next pass's twiddles between the exchange stores and the barrier
+#endif
 template <class Cfg, int P, bool FREE_EARLY, class Release, class Free>
 __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
                                           const typename Cfg::C* __restrict__ tw, Release&& release,
-                                          Free&& free_hook) {
+                                          Free&& free_hook, typename Cfg::C (&wpre)[Cfg::E]) {
   using C = typename Cfg::C;
   constexpr int E = Cfg::E, TR = Cfg::TR;
   constexpr int R = (P == 0) ? Cfg::R0 : E;
@@ -333,7 +336,9 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
       const C* twp = tw + Cfg::twoff(P) + k;
 #pragma unroll
       for (int t = 1; t < R; ++t) {
-        C w = __ldg(twp + (t - 1) * NS);
+        C w;
+        if constexpr (XFT_TWPRE && P >= 1 && NB == 1) w = wpre[t - 1];  // loaded under the previous barrier
+        else w = __ldg(twp + (t - 1) * NS);
         if (Cfg::SIGN > 0) w = cconj(w);
         u[t] = cmul(u[t], w);
       }
@@ -357,6 +362,16 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
 #pragma unroll
       for (int t = 0; t < R; ++t) dst[t * NS + ((t * NS) >> 4)] = v[b + t * NB];
     }
+    if constexpr (XFT_TWPRE && XFT_SKELETON == 0 && !XFT_NOTW) {
+      // v is dead until the loads below: its registers carry the next pass's twiddles
+      // across the barrier, so their L1/L2 latency overlaps the wait
+      constexpr int NS1 = Cfg::ns(P + 1);
+      if constexpr (NS1 > 1 && E / E == 1) {
+        const C* twp = tw + Cfg::twoff(P + 1) + (j & (NS1 - 1));
+#pragma unroll
+        for (int t = 1; t < E; ++t) wpre[t - 1] = __ldg(twp + (t - 1) * NS1);
+      }
+    }
     __syncthreads();
     // j < TR and TR | 16 or 16 | TR: pad_idx(j + s TR) = pad_idx(j) + s TR + (s TR) / 16
     const C* src = rs + pad_idx(j);
@@ -369,14 +384,22 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
   }
 }
 
+template <class Cfg, int P, bool FREE_EARLY, class Release, class Free>
+__device__ __forceinline__ void pipe_passes_w(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
+                                              const typename Cfg::C* __restrict__ tw, Release&& release,
+                                              Free&& free_hook, typename Cfg::C (&wpre)[Cfg::E]) {
+  if constexpr (P < Cfg::NPASS) {
+    pipe_pass<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre);
+    pipe_passes_w<Cfg, P + 1, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre);
+  }
+}
+
 template <class Cfg, int P, bool FREE_EARLY = false, class Release, class Free>
 __device__ __forceinline__ void pipe_passes(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
                                             const typename Cfg::C* __restrict__ tw, Release&& release,
                                             Free&& free_hook) {
-  if constexpr (P < Cfg::NPASS) {
-    pipe_pass<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook);
-    pipe_passes<Cfg, P + 1, FREE_EARLY>(v, rs, j, tw, release, free_hook);
-  }
+  typename Cfg::C wpre[Cfg::E];
+  pipe_passes_w<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre);
 }
 
 template <class Cfg, int P, class Release>
