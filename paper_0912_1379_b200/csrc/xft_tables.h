@@ -36,8 +36,12 @@ struct Tables {
 int get_tables(int64_t n, int dtype, Tables* out, int radix = -1);
 
 // radix of the in-CTA chirp-z kernels for an FFT of length 2^l
+#ifndef XFT_BLUE_E13
+#define XFT_BLUE_E13 16  // radix of the c128 M = 8192 chirp-z / Mehler CTA (32: 256 threads)
+#endif
 constexpr int blue_radix(int dtype, int l) {
-  return pipe_radix(dtype, l) < (1 << (l - 1)) ? pipe_radix(dtype, l) : (1 << (l - 1));
+  return (dtype == 1 && l == 13) ? XFT_BLUE_E13
+         : pipe_radix(dtype, l) < (1 << (l - 1)) ? pipe_radix(dtype, l) : (1 << (l - 1));
 }
 
 // Host formulas shared with the C-ABI.
