@@ -422,7 +422,7 @@ def run_ours(args, rank, world, local_rank):
             per[it.tag]["frac_of_hbm_nvlink_roofline"] = t_roof * 1e3 / kern_ms[k]
     dom = max(per, key=lambda t: per[t]["kernel_ms"])
     kname = {"lct": "xft_pipe_kernel", "mehler": "xft_blue_kernel + xft_tile_kernel",
-             "lct2d": "xft_pipe_kernel + xft_tile_kernel"}[work[[it.tag for it in work].index(dom)].kind]
+             "lct2d": "xft_pipe_kernel + xft_colclu_kernel"}[work[[it.tag for it in work].index(dom)].kind]
     roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
             "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"{kname} {dom}",
             "peak_source": peak_kind,
