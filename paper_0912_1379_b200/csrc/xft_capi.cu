@@ -230,6 +230,9 @@ int launch_transpose(const void* in, void* out, int64_t rows, int64_t cols, int6
 
 }  // namespace
 
+#ifndef XFT_HOST_CHUNK_MB
+#define XFT_HOST_CHUNK_MB 16  // host-path chunk (H2D / kernel / D2H pipeline granularity)
+#endif
 namespace {
 // persistent resources of the host-buffer path (xft_lct_host), one per device
 struct HostPipe {
@@ -396,7 +399,7 @@ int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype,
   const size_t row_bytes = esz * (size_t)n;
   // chunk ~ 16 MiB, at least one row; 3 slots rotate over 3 streams so the
   // H2D of chunk c+1, the kernel of chunk c and the D2H of chunk c-1 overlap.
-  int64_t chunk = (int64_t)((16u << 20) / row_bytes);
+  int64_t chunk = (int64_t)(((size_t)XFT_HOST_CHUNK_MB << 20) / row_bytes);
   if (chunk < 1) chunk = 1;
   if (chunk > batch) chunk = batch;
   int dev = 0;
