@@ -9,6 +9,9 @@ namespace xftb {
 
 // Radix (elements per thread) of the pipelined kernel for (dtype, log2 n);
 // shared by the host table builder and the kernel instantiation.
+#ifndef XFT_C64_E10
+#define XFT_C64_E10 32  // radix of the n = 512, 1024 c64 rows: 32 = two passes, one exchange (cfg4 232 -> 191 us)
+#endif
 #ifndef XFT_C64_E14
 #define XFT_C64_E14 32  // radix of the n = 16384 c64 rows (16: 1024 threads, 4 passes)
 #endif
@@ -21,7 +24,7 @@ namespace xftb {
 #endif
 constexpr int C128_TABN = 1 << XFT_C128_TABL;
 constexpr int pipe_radix(int dtype, int l) {
-  return dtype == 0 ? (l >= 14 ? XFT_C64_E14 : 16) : (l >= 13 ? 16 : XFT_C128_E);
+  return dtype == 0 ? (l >= 14 ? XFT_C64_E14 : (l == 9 || l == 10) ? XFT_C64_E10 : 16) : (l >= 13 ? 16 : XFT_C128_E);
 }
 
 struct Tables {
