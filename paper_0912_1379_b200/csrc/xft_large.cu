@@ -805,7 +805,10 @@ int lct_cols_narrow(const void* in, void* out, void* ws, int64_t R, int64_t ncol
 // is written, groups are disjoint.
 // ---------------------------------------------------------------------------
 #ifndef XFT_CLU14
-#define XFT_CLU14 1  // R = 16384: 0 = 16-CTA clusters x 1024 rows, 1 = 8-CTA clusters x 2048 rows (half-width groups)
+#define XFT_CLU14 0  // R = 16384: 0 = 16-CTA clusters x 1024 rows, 1 = 8-CTA clusters x 2048 rows (half-width groups)
+#endif
+#ifndef XFT_CLU_E10
+#define XFT_CLU_E10 32  // c64 radix of the 1024-row cluster slices (32: two passes, one warp per column)
 #endif
 #ifndef XFT_CLU_PROMO
 #define XFT_CLU_PROMO 0  // L2 promotion of the column-group TMA loads (bytes; 0 = none)
@@ -873,7 +876,8 @@ template <class C_, int K_, int LOGL_, int W_, int NBUF_, int MINB_>
 struct CluCfg {
   using C = C_;
   static constexpr int K = K_, LOGL = LOGL_, W = W_, NBUF = NBUF_, MINB = MINB_;
-  static constexpr int L = 1 << LOGL, E = 16, TR = L / E, THREADS = W * TR;
+  static constexpr int L = 1 << LOGL, E = (sizeof(C) == 8 && LOGL == 10) ? XFT_CLU_E10 : 16, TR = L / E,
+                       THREADS = W * TR;
   using Fft = PipeCfg<C, LOGL, E, MODE_DFT, -1, W, 1, 1>;
   // line stride: a 128-byte wavefront covers S = 128/sizeof(C) lanes = W lines x S/W
   // consecutive positions; LS = S/W (mod S) puts them in S distinct slots
