@@ -41,13 +41,14 @@ xft_chain_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __rest
   void* tab = xft_smem + size_t(Cfg::STAGE) * sizeof(C);
   const int tid = threadIdx.x, lrow = tid / TR, j = tid - lrow * TR;
   const ThreadConst<Cfg> tc(j);
-  if (tid < cp.nst) make_coef(cs[tid], nullptr, cp.st[tid], kc);
   if constexpr (Cfg::C128) {
     double2* t = static_cast<double2*>(tab);
     const double2* g = static_cast<const double2*>(gtab);
     for (int m = tid; m < XFT_C128_TABCOPIES * C128_TABN; m += Cfg::THREADS)
       t[m] = g[XFT_C128_TABCOPIES == 8 ? m >> 3 : m];
+    __syncthreads();  // make_coef reads the table
   }
+  if (tid < cp.nst) make_coef(cs[tid], nullptr, cp.st[tid], kc, TR, static_cast<const double2*>(tab));
   __syncthreads();
   auto noop = []() {};
   const long long ntiles = (batch + ROWS - 1) / ROWS;

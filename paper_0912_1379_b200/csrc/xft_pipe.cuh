@@ -91,9 +91,14 @@ struct __align__(16) Coef128 {
   double cin, cout, s4;  // fl(0.5a/b), fl(0.5d/b), fl(4b/pi)
   double gabs, gf;       // |G|, small part of arg G (|gf| <= U/2)
   double2 g;             // G (used when d == 0)
+  // walk path: the chirp phase without the reference's roundings, in turns per
+  // m^2 (m = 2k - n + 1), as double-doubles: cin half^2 / 2pi, cout s4^2 half^2 / 2pi
+  double din_hi, din_lo, dout_hi, dout_lo;
+  double2 sin_, sout;    // second-difference phasors e^{2 pi i D (2 TR)^2 2}
+  double gturn;          // arg G in turns (exact)
   int gi;                // arg G / U rounded (table units)
-  int pre, post;         // chirp present (0 = none, 1 = table path, 2 = huge phase)
-  int pad[3];
+  int pre, post;         // 0 none, 1 walk, 2 walk + rounding correction, 3 table, 4 table + pre-reduction
+  int pad;
 };
 static_assert(sizeof(Coef64) % 16 == 0 && sizeof(Coef128) % 16 == 0, "bulk-copy granularity");
 
@@ -125,7 +130,8 @@ __device__ __forceinline__ double g_abs(double b, const RowConst& k) {
   return g;
 }
 
-__device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd& uni, const RowConst& k) {
+__device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd& uni, const RowConst& k, int,
+                                          const double2*) {
   double a, b, d;
   row_params(p, uni, a, b, d);
   const double cin = __ddiv_rn(0.5 * a, b), cout = __ddiv_rn(0.5 * d, b), s4 = __ddiv_rn(4.0 * b, XFT_PI);
@@ -146,7 +152,57 @@ __device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd
   c.post = (d != 0.0);
 }
 
-__device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abcd& uni, const RowConst& k) {
+// ---- c128 chirp walk helpers -------------------------------------------------
+#ifndef XFT_C128_WALK
+#define XFT_C128_WALK 1  // 0: every c128 chirp through the per-element table path (modes 3/4)
+#endif
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_norm(double s, double e) {  // fast two-sum, |s| >= |e|
+  const double h = __dadd_rn(s, e);
+  return DD{h, __dsub_rn(e, __dsub_rn(h, s))};
+}
+__device__ __forceinline__ DD dd_prod(double a, double b) {
+  const double p = __dmul_rn(a, b);
+  return DD{p, fma(a, b, -p)};
+}
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  const DD p = dd_prod(a.hi, b.hi);
+  return dd_norm(p.hi, fma(a.hi, b.lo, fma(a.lo, b.hi, p.lo)));
+}
+__device__ __forceinline__ DD dd_mul(DD a, double b) {
+  const DD p = dd_prod(a.hi, b);
+  return dd_norm(p.hi, fma(a.lo, b, p.lo));
+}
+
+// frac(D M) for a double-double D and an exact integer-valued M (|M| < 2^53):
+// f = a - rint(a) exactly (|f| <= 1/2) and the low part lo, D M = f + lo (mod 1)
+__device__ __forceinline__ void frac_dd(double dhi, double dlo, double M, double& f, double& lo) {
+  const double a = __dmul_rn(dhi, M);
+  lo = fma(dlo, M, fma(dhi, M, -a));
+  f = __dsub_rn(a, rint(a));
+}
+
+// e^{2 pi i (f + lin + lo)} from the c128 table: f exact with |f| <= 1/2, lin a
+// short multiple of 2^-16 (|lin| <= 2), lo small.  The table quantum q is taken
+// out of f + lin exactly (Sterbenz) before the low part is added, so the
+// argument is accurate to ~1e-18 turn whatever the magnitude of the phase was.
+__device__ __forceinline__ double2 turn_phasor(double f, double lin, double lo, const double2* __restrict__ tab) {
+  const double t = fma(__dadd_rn(f, lin), (double)C128_TABN, 6755399441055744.0);
+  const double qd = __dsub_rn(t, 6755399441055744.0);
+  const int q = __double2loint(t);
+  const double g = __dadd_rn(__dadd_rn(f, fma(-qd, 1.0 / C128_TABN, lin)), lo);
+  const double r = __dmul_rn(g, 6.283185307179586);
+  const double z = r * r;
+  const double sn = fma(r * z, fma(z, kC128[4], kC128[3]), r);
+  const double cs = fma(z, fma(z, fma(z, kC128[7], kC128[6]), kC128[5]), 1.0);
+  const double2 w = tab[q & (C128_TABN - 1)];
+  return make_double2(w.x * cs - w.y * sn, w.x * sn + w.y * cs);
+}
+
+__device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abcd& uni, const RowConst& k, int tr,
+                                          const double2* __restrict__ tab) {
   double a, b, d;
   row_params(p, uni, a, b, d);
   c.cin = __ddiv_rn(0.5 * a, b);      // (0.5j * a / b).imag     xft/kernel.py:102
@@ -159,18 +215,38 @@ __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abc
   const double vi = rint(v);
   c.gi = (int)vi;
   c.gf = (v - vi) * kC128[0];
+  c.gturn = v * (1.0 / C128_TABN);
   c.gabs = g_abs(b, k);
   double s, co;
   sincospi(v * (2.0 / C128_TABN), &s, &co);
   c.g = make_double2(c.gabs * co, c.gabs * s);
-  // largest |phase| on the row = |coef| x_max^2; the table reduction is exact
-  // for |phi| < ~1e13, beyond 1e11 the row takes the full-range sincos path
+  // smooth chirp rates (turns per m^2) and the walk's second-difference phasors
+  const DD h2i = dd_mul(dd_prod(k.half, k.half), DD{0.15915494309189535, -9.839338337591243e-18});
+  const DD din = dd_mul(h2i, c.cin);
+  const DD dout = dd_mul(dd_mul(dd_prod(c.s4, c.s4), c.cout), h2i);
+  c.din_hi = din.hi; c.din_lo = din.lo; c.dout_hi = dout.hi; c.dout_lo = dout.lo;
+  const double m2 = 8.0 * (double)tr * (double)tr;  // (2 tr)^2 * 2, a power of two: exact scaling
+  double f, lo;
+  frac_dd(din.hi, din.lo, m2, f, lo);
+  c.sin_ = turn_phasor(f, 0.0, lo, tab);
+  frac_dd(dout.hi, dout.lo, m2, f, lo);
+  c.sout = turn_phasor(f, 0.0, lo, tab);
+  // largest |phase| on the row = |coef| x_max^2.  Below 2^11 rad the reference's
+  // argument roundings stay under 1.1e-13 rms per row and the smooth walk is
+  // used as is; below 2^24 the rounding error is re-added per element to first
+  // order (|eps| < 1e-8); the table path is exact for |phi| < ~1e13, beyond
+  // 1e12 the row is pre-reduced.
   const double x2 = (double)((1ll << k.log2n) - 1) * k.half;
   const double pmax_in = fabs(c.cin) * x2 * x2;
   const double y2 = fabs(c.s4) * x2;
   const double pmax_out = fabs(c.cout) * y2 * y2;
-  c.pre = (a != 0.0) ? (pmax_in < 1e12 ? 1 : 2) : 0;
-  c.post = (d != 0.0) ? (pmax_out < 1e12 ? 1 : 2) : 0;
+  auto mode_of = [](double pm) {
+    if (XFT_C128_WALK && pm < 2048.0) return 1;
+    if (XFT_C128_WALK && pm < 16777216.0) return 2;
+    return pm < 1e12 ? 3 : 4;
+  };
+  c.pre = (a != 0.0) ? mode_of(pmax_in) : 0;
+  c.post = (d != 0.0) ? mode_of(pmax_out) : 0;
 #ifdef XFT_NOCHIRP  // tuning only: time the kernel with the chirps replaced by the p_k table path
   c.pre = (XFT_NOCHIRP & 1) ? 0 : c.pre;
   c.post = (XFT_NOCHIRP & 2) ? 0 : c.post;
@@ -309,6 +385,9 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 // FREE_EARLY: after the last exchange's reads, one more barrier and free_hook()
 // -- the buffer is dead from there on, so a single-stage caller can start the
 // next tile's load under the last pass and the epilogue.
+#ifndef XFT_TWGEN
+#define XFT_TWGEN 1  // c64 inter-pass twiddles generated from two table entries per butterfly (0: all R-1 loaded)
+#endif
 #ifndef XFT_TWPRE
 #define XFT_TWPRE 0  // 1: load the next pass's twiddles between the exchange stores and the barrier
 #endif
@@ -332,7 +411,22 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
 #ifndef XFT_NOTW
 #define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
 #endif
-    if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW) {
+    if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW && XFT_TWGEN && !Cfg::C128 && R >= 8) {
+      // c64: w^t = w^{t-1} w for t != 8, w and w^8 from the table: two loads
+      // instead of R - 1 (cfg4 191 -> 182 us); error <= 7 fp32 rounding steps per
+      // twiddle.  c128 keeps the table (no gain measured, and the long Mehler
+      // convolutions would lose ~1e-14)
+      const C* twp = tw + Cfg::twoff(P) + k;
+      C w1 = __ldg(twp), w8 = __ldg(twp + 7 * NS);
+      if (Cfg::SIGN > 0) { w1 = cconj(w1); w8 = cconj(w8); }
+      C w = w1;
+      u[1] = cmul(u[1], w1);
+#pragma unroll
+      for (int t = 2; t < R; ++t) {
+        w = (t == 8) ? w8 : cmul(w, w1);
+        u[t] = cmul(u[t], w);
+      }
+    } else if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW) {
       const C* twp = tw + Cfg::twoff(P) + k;
 #pragma unroll
       for (int t = 1; t < R; ++t) {
@@ -433,14 +527,72 @@ struct ThreadConst<Cfg, true> {
   static constexpr int H = C128_TABN / 2;
   double d0;
   int q0;
+  // walk path: the boundary phase at k = j in turns, (n-1) j / 2n mod 1 (exact)
+  double lin0;
   __device__ __forceinline__ explicit ThreadConst(int j) {
     off0 = opaque((double)(2 * j - Cfg::N + 1));
+    lin0 = opaque(0.5 * (double)(j & 1) - (double)j / (double)(2 * Cfg::N));
     const int jq = (H * j + Cfg::N / 2) / Cfg::N;  // nearest integer to H j / n
     d0 = opaque(-(double)(H * j - jq * Cfg::N) * (6.283185307179586477 / (double(C128_TABN) * Cfg::N)));
     q0 = (j & 1) * H - jq;
   }
   static constexpr int qstep(int s) { return -(H / Cfg::E) * s; }
 };
+
+// c128 chirp walk over a thread's elements k = j + s TR (m = m0 + 2 TR s):
+// the smooth phase D m^2 + (boundary/constant turns) is a quadratic in s, so
+// W(s+1) = W(s) R(s), R(s+1) = R(s) S with W(0), R(0) from the table path
+// (exact double-double arguments) and S per row.  Two complex multiplies per
+// element, no table loads; |error| < ~2e-14 after 15 steps.
+struct ChirpWalk {
+  double2 W, R;
+  template <class Cfg>
+  __device__ __forceinline__ void init(double dhi, double dlo, const ThreadConst<Cfg>& tc, double lin, double mag,
+                                       const double2* __restrict__ tab) {
+    constexpr int TR = Cfg::TR;
+    const double m0 = tc.off0;
+    double f, lo;
+    frac_dd(dhi, dlo, m0 * m0, f, lo);
+    W = turn_phasor(f, lin, lo, tab);
+    W.x *= mag;
+    W.y *= mag;
+    // R(0): D ((m0 + 2TR)^2 - m0^2) + one step of the boundary phase, (n-1) TR / 2n = -1/2E (mod 1)
+    frac_dd(dhi, dlo, (double)(4 * TR) * (m0 + (double)TR), f, lo);
+    R = turn_phasor(f, -0.5 / Cfg::E, lo, tab);
+  }
+  __device__ __forceinline__ void step(const double2& S, bool moveR) {
+    W = make_double2(W.x * R.x - W.y * R.y, W.x * R.y + W.y * R.x);
+    if (moveR) R = make_double2(R.x * S.x - R.y * S.y, R.x * S.y + R.y * S.x);
+  }
+};
+
+// e^{i eps} ~ 1 + i eps applied to w: the reference's argument roundings,
+// eps = fl(c fl(x^2)) - c X^2, x = fl(X), X = m half (xft/kernel.py:102, xft/hermite.py:87-89)
+__device__ __forceinline__ double2 rot_eps(double2 w, double eps) {
+  return make_double2(fma(-w.y, eps, w.x), fma(w.x, eps, w.y));
+}
+__device__ __forceinline__ double pre_eps(double m, double half, double c, double c2) {
+  const double x = __dmul_rn(m, half);
+  const double ex = fma(m, half, -x);   // X = x + ex
+  const double x2 = __dmul_rn(x, x);
+  const double e2 = fma(x, x, -x2);     // x^2 = x2 + e2
+  const double ph = __dmul_rn(c, x2);   // the reference's phase
+  const double ep = fma(-c, x2, ph);    // ph - c x2
+  // ph - c X^2 = ep - c e2 - 2 c x ex  (- c ex^2, below 1e-25)
+  return fma(c2, __dmul_rn(x, ex), fma(-c, e2, ep));
+}
+// output side: y = fl(s4 x), psi = fl(cout fl(y^2)) (xft/lct.py:196, xft/kernel.py:113), Y = s4 X
+__device__ __forceinline__ double post_eps(double m, double half, double s4, double c, double c2) {
+  const double x = __dmul_rn(m, half);
+  const double ex = fma(m, half, -x);
+  const double y = __dmul_rn(s4, x);
+  const double dy = fma(s4, ex, fma(s4, x, -y));  // Y = y + dy
+  const double y2 = __dmul_rn(y, y);
+  const double e2 = fma(y, y, -y2);
+  const double ps = __dmul_rn(c, y2);
+  const double ep = fma(-c, y2, ps);
+  return fma(c2, __dmul_rn(y, dy), fma(-c, e2, ep));
+}
 
 // ---------------------------------------------------------------------------
 // pre / post multipliers over a thread's E registers (row-uniform branches
@@ -475,7 +627,26 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], Load&& l
       } else {
         const double2* tab = static_cast<const double2*>(tabv);
         const double cin = rcs.cin, half = kc.half;
-        if (mode == 1) {
+        if (mode <= 2) {
+          ChirpWalk w;
+          w.init<Cfg>(rcs.din_hi, rcs.din_lo, tc, tc.lin0, 1.0, tab);
+          const double2 S = rcs.sin_;
+          if (mode == 1) {
+#pragma unroll
+            for (int s = 0; s < E; ++s) {
+              v[s] = cmul(w.W, ld(s));
+              if (s < E - 1) w.step(S, s < E - 2);
+            }
+          } else {
+            const double c2 = -2.0 * cin;
+#pragma unroll
+            for (int s = 0; s < E; ++s) {
+              const double eps = pre_eps(tc.off0 + (double)(2 * s * TR), half, cin, c2);
+              v[s] = cmul(rot_eps(w.W, eps), ld(s));
+              if (s < E - 1) w.step(S, s < E - 2);
+            }
+          }
+        } else if (mode == 3) {
 #pragma unroll
           for (int s = 0; s < E; ++s) {
             const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);  // xft/hermite.py:87-89
@@ -549,7 +720,26 @@ __device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, 
       const double cout = rcs.cout, s4 = rcs.s4, half = kc.half, g = rcs.gabs;
       const double d0 = tc.d0 + rcs.gf;
       const int q0 = tc.q0 + rcs.gi;
-      if (rcs.post == 1) {
+      if (rcs.post <= 2) {
+        ChirpWalk w;
+        w.init<Cfg>(rcs.dout_hi, rcs.dout_lo, tc, tc.lin0 + rcs.gturn, g, tab);
+        const double2 S = rcs.sout;
+        if (rcs.post == 1) {
+#pragma unroll
+          for (int s = 0; s < E; ++s) {
+            emit(s, cmul(w.W, v[s]));
+            if (s < E - 1) w.step(S, s < E - 2);
+          }
+        } else {
+          const double c2 = -2.0 * cout;
+#pragma unroll
+          for (int s = 0; s < E; ++s) {
+            const double eps = post_eps(tc.off0 + (double)(2 * s * TR), half, s4, cout, c2);
+            emit(s, cmul(rot_eps(w.W, eps), v[s]));
+            if (s < E - 1) w.step(S, s < E - 2);
+          }
+        }
+      } else if (rcs.post == 3) {
 #pragma unroll
         for (int s = 0; s < E; ++s) {
           const double x = __dmul_rn(tc.off0 + (double)(2 * s * TR), half);
@@ -630,7 +820,8 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     if constexpr (Cfg::MODE == MODE_LCT) {
       for (int idx = threadIdx.x; idx < CH * ROWS; idx += Cfg::THREADS) {
         const long long row = (first_tile + (long long)(idx / ROWS) * G) * ROWS + idx % ROWS;
-        if (row < batch) make_coef(coeft[idx / ROWS][idx % ROWS], abcd ? abcd + row * abcd_stride : nullptr, uni, kc);
+        if (row < batch) make_coef(coeft[idx / ROWS][idx % ROWS], abcd ? abcd + row * abcd_stride : nullptr, uni, kc, Cfg::TR,
+                                static_cast<const double2*>(tab));
       }
     }
   };

@@ -144,6 +144,26 @@ def test_config2_full_batch(torch, X, dtype, tol):
     assert np.max(np.abs(lhs / rhs - 1)) <= (1e-12 if dtype == np.complex128 else 1e-4)
 
 
+@pytest.mark.parametrize("n", [64, 1024, 4096, 8192])
+def test_c128_chirp_modes(torch, X, n):
+    """c128 rows whose largest chirp phase puts each side in every evaluation mode:
+    smooth walk (< 2^11 rad), walk + per-element rounding correction (< 2^24),
+    table (< 1e12), pre-reduced table (beyond), and a = 0 / d = 0 rows."""
+    rows = []
+    for al in (math.pi / 2, 1.3, 0.3, 3.02e-4, math.pi - 6.56e-4, 1e-6, 1e-10):
+        rows.append((math.cos(al), math.sin(al), -math.sin(al), math.cos(al)))
+    for a, b, d in ((2.0, 1.0, 2000.0), (0.5, 1.0, 1e6), (3.0, 1.0, 1e10), (1e8, 1.0, 0.0), (0.0, 1.0, 1e7),
+                    (-2.5, -0.7, 33.0)):
+        rows.append((a, b, (a * d - 1.0) / b, d))
+    abcd = np.array(rows, dtype=np.float64)
+    rng = np.random.default_rng(11)
+    f = (rng.standard_normal((len(rows), n)) + 1j * rng.standard_normal((len(rows), n))) / math.sqrt(2)
+    got = X.ops.lct_rows(dev(torch, f), abcd).cpu().numpy()
+    _, ref = O.fast_lct_rows(abcd, f)
+    err = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert np.max(err) <= TOL128, err
+
+
 def test_config4_full_batch_and_quadrature(torch, X):
     from paper_0912_1379_b200 import workloads
 
