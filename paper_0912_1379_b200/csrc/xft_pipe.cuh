@@ -639,9 +639,10 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], Load&& l
             }
           } else {
             const double c2 = -2.0 * cin;
+            const double o = opaque(tc.off0);  // per tile: keeps the 16 m's from being hoisted (and spilled)
 #pragma unroll
             for (int s = 0; s < E; ++s) {
-              const double eps = pre_eps(tc.off0 + (double)(2 * s * TR), half, cin, c2);
+              const double eps = pre_eps(o + (double)(2 * s * TR), half, cin, c2);
               v[s] = cmul(rot_eps(w.W, eps), ld(s));
               if (s < E - 1) w.step(S, s < E - 2);
             }
@@ -732,9 +733,10 @@ __device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, 
           }
         } else {
           const double c2 = -2.0 * cout;
+          const double o = opaque(tc.off0);
 #pragma unroll
           for (int s = 0; s < E; ++s) {
-            const double eps = post_eps(tc.off0 + (double)(2 * s * TR), half, s4, cout, c2);
+            const double eps = post_eps(o + (double)(2 * s * TR), half, s4, cout, c2);
             emit(s, cmul(rot_eps(w.W, eps), v[s]));
             if (s < E - 1) w.step(S, s < E - 2);
           }
