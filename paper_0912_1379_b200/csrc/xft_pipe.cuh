@@ -386,7 +386,7 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 // -- the buffer is dead from there on, so a single-stage caller can start the
 // next tile's load under the last pass and the epilogue.
 #ifndef XFT_TWGEN
-#define XFT_TWGEN 1  // c64 inter-pass twiddles generated from two table entries per butterfly (0: all R-1 loaded)
+#define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
 #endif
 #ifndef XFT_TWPRE
 #define XFT_TWPRE 0  // 1: load the next pass's twiddles between the exchange stores and the barrier
@@ -411,11 +411,12 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
 #ifndef XFT_NOTW
 #define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
 #endif
-    if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW && XFT_TWGEN && !Cfg::C128 && R >= 8) {
-      // c64: w^t = w^{t-1} w for t != 8, w and w^8 from the table: two loads
-      // instead of R - 1 (cfg4 191 -> 182 us); error <= 7 fp32 rounding steps per
-      // twiddle.  c128 keeps the table (no gain measured, and the long Mehler
-      // convolutions would lose ~1e-14)
+    if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW && XFT_TWGEN && (!Cfg::C128 || Cfg::MODE != MODE_DFT) && R >= 8) {
+      // w^t = w^{t-1} w for t != 8, w and w^8 from the table: two loads instead
+      // of R - 1 (fewer registers held by in-flight loads; cfg4 191 -> 182 us,
+      // cfg2 c128 129.2 -> 127.6 us); error <= 7 rounding steps per twiddle.
+      // The plain-DFT configurations (chirp-z / Mehler convolutions, up to
+      // 2^17 points) keep the exact table twiddles.
       const C* twp = tw + Cfg::twoff(P) + k;
       C w1 = __ldg(twp), w8 = __ldg(twp + 7 * NS);
       if (Cfg::SIGN > 0) { w1 = cconj(w1); w8 = cconj(w8); }
