@@ -92,7 +92,7 @@ struct PipeShape {
 template <class C, int L, int MODE, int SIGN>
 int launch_pipe(const LaunchArgs& a) {
   using SH = PipeShape<C, L>;
-  using Cfg = PipeCfg<C, L, SH::E, MODE, SIGN, SH::ROWS, SH::STAGES, SH::MINB>;
+  using Cfg = PipeCfg<C, L, SH::E, MODE, SIGN, SH::ROWS, SH::STAGES, SH::MINB, 1>;
   auto kern = xft_pipe_kernel<Cfg>;
   static int occ_cache[64] = {0};
   int dev = 0;

@@ -45,6 +45,10 @@
 #endif
 #include "xft_tma.cuh"
 
+#ifndef XFT_SPLIT
+#define XFT_SPLIT 1  // split next-row prefetch for single-row CTAs (see PipeCfg::SPLIT)
+#endif
+
 #ifndef XFT_SKELETON
 #define XFT_SKELETON 0  // tuning only: 1 = exchanges without math, 2 = pure copy
 #endif
@@ -347,7 +351,7 @@ struct TurnWalk {
 // ---------------------------------------------------------------------------
 // configuration
 // ---------------------------------------------------------------------------
-template <class C_, int LOG2N_, int E_, int MODE_, int SIGN_, int ROWS_, int STAGES_, int MINB_>
+template <class C_, int LOG2N_, int E_, int MODE_, int SIGN_, int ROWS_, int STAGES_, int MINB_, int SPLITOK_ = 0>
 struct PipeCfg {
   using C = C_;
   using Coef = typename CoefOf<C>::T;
@@ -367,7 +371,17 @@ struct PipeCfg {
   static constexpr int R0 = 1 << (LOG2N - (NPASS - 1) * LE);
   static constexpr bool C128 = sizeof(C) == 16;
   static constexpr size_t TAB_BYTES = C128 ? XFT_C128_TABCOPIES * C128_TABN * sizeof(double2) : 0;
-  static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(C) + TAB_BYTES;
+  // One resident single-row CTA per SM (rows of 128 KB) cannot double-buffer
+  // its tile, so the spare shared memory becomes a landing region for the first
+  // SPLIT samples of the next row, loaded as soon as this row's input has been
+  // read (first exchange barrier); the rest of the next row lands in the stage
+  // once the last exchange has been read.  SPLIT is a multiple of TR.
+  static constexpr size_t SMEM_MAX = 232448 - 8192;  // 227 KB opt-in minus static shared memory
+  static constexpr size_t MAIN = size_t(STAGES) * STAGE * sizeof(C) + TAB_BYTES;
+  static constexpr int SPLIT0 = (SPLITOK_ && ROWS == 1 && STAGES == 1 && MINB_ == 1 && XFT_SPLIT && SMEM_MAX > MAIN)
+                                    ? int((SMEM_MAX - MAIN) / sizeof(C)) / TR * TR : 0;
+  static constexpr int SPLIT = SPLIT0 < N ? SPLIT0 : 0;
+  static constexpr size_t SMEM = MAIN + size_t(SPLIT) * sizeof(C);
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
   static_assert(THREADS <= 1024, "threads");
@@ -804,6 +818,8 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
 
   C* stage0 = reinterpret_cast<C*>(xft_smem);
   void* tab = xft_smem + size_t(S) * Cfg::STAGE * sizeof(C);
+  constexpr int SPLIT = Cfg::SPLIT;
+  C* const regA = reinterpret_cast<C*>(xft_smem + Cfg::MAIN);  // samples [0, SPLIT) of the row (split mode)
 
   const int tid = threadIdx.x;
   const int lrow = tid / Cfg::TR;
@@ -819,6 +835,18 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     mbar_arrive_expect_tx(&bars[st], bytes);
     tma_load_1d(stage0 + size_t(st) * Cfg::STAGE, in + (XFT_NOMEM ? (long long)blockIdx.x : t) * Cfg::TILE, bytes, &bars[st]);
   };
+  // split mode (ROWS == 1): part A = samples [0, SPLIT) -> regA, part B = the rest -> the stage
+  auto issue_a = [&](long long t) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[0], (uint32_t)(SPLIT * sizeof(C)));
+    tma_load_1d(regA, in + (XFT_NOMEM ? (long long)blockIdx.x : t) * Cfg::TILE, (uint32_t)(SPLIT * sizeof(C)), &bars[0]);
+  };
+  auto issue_b = [&](long long t) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[0], (uint32_t)((N - SPLIT) * sizeof(C)));
+    tma_load_1d(stage0 + SPLIT, in + (XFT_NOMEM ? (long long)blockIdx.x : t) * Cfg::TILE + SPLIT,
+                (uint32_t)((N - SPLIT) * sizeof(C)), &bars[0]);
+  };
   auto fill_coefs = [&](long long first_tile) {  // tiles first_tile + q*G, q < CH
     if constexpr (Cfg::MODE == MODE_LCT) {
       for (int idx = threadIdx.x; idx < CH * ROWS; idx += Cfg::THREADS) {
@@ -831,7 +859,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
 
   // ---- prologue ----
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], SPLIT ? 2 : 1);  // split: one arrival per part
     fence_mbar_init();
   }
   if constexpr (Cfg::C128) {
@@ -845,7 +873,14 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   if (tid == 0) {
     for (int s = 0; s < S - 1; ++s)
       if (tile + s * G < ntiles) issue(tile + s * G, s);
-    if (S == 1 && tile < ntiles) issue(tile, 0);
+    if (S == 1 && tile < ntiles) {
+      if constexpr (SPLIT > 0) {
+        issue_a(tile);
+        issue_b(tile);
+      } else {
+        issue(tile, 0);
+      }
+    }
   }
 
   for (int it = 0; tile < ntiles; ++it, tile += G) {
@@ -876,6 +911,10 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     if constexpr (XFT_SKELETON) {
 #pragma unroll
       for (int s = 0; s < Cfg::E; ++s) v[s] = rs[j + s * Cfg::TR];
+    } else if constexpr (SPLIT > 0) {
+      // element s of this thread lives in part A iff s TR + j < SPLIT, i.e. s < SPLIT / TR
+      pre_apply<Cfg>(v, [&](int s) { return (s < SPLIT / Cfg::TR ? regA : rs)[j + s * Cfg::TR]; }, j, rc, tc, kc,
+                     ptab, tab);
     } else {
       pre_multiply<Cfg>(v, rs, j, rc, tc, kc, ptab, tab);
     }
@@ -886,13 +925,19 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
         const long long nt = tile + (S - 1) * G;
         if (nt < ntiles) issue(nt, (it + S - 1) % S);
       }
+      if constexpr (SPLIT > 0) {  // part A of this row has been read: start the next row's part A
+        if (tid == 0 && tile + G < ntiles) issue_a(tile + G);
+      }
     };
     // single stage: the next tile's load starts once the last exchange has been
     // read (c64; for c128 the barrier in front of the fp64-heavy last pass
     // costs more than the earlier load gains, measured 137 -> 146 us at cfg2)
     constexpr bool EARLY = S == 1 && !Cfg::C128;
     auto stage_free = [&]() {
-      if (tid == 0 && tile + G < ntiles) issue(tile + G, 0);
+      if (tid == 0 && tile + G < ntiles) {
+        if constexpr (SPLIT > 0) issue_b(tile + G);
+        else issue(tile + G, 0);
+      }
     };
     if constexpr (XFT_SKELETON == 2) {
       __syncthreads();
