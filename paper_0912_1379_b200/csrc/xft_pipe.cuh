@@ -426,20 +426,33 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
 #define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
 #endif
     if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW && XFT_TWGEN && (!Cfg::C128 || Cfg::MODE != MODE_DFT) && R >= 8) {
-      // w^t = w^{t-1} w for t != 8, w and w^8 from the table: two loads instead
-      // of R - 1 (fewer registers held by in-flight loads; cfg4 191 -> 182 us,
-      // cfg2 c128 129.2 -> 127.6 us); error <= 7 rounding steps per twiddle.
+      // w^t from w and w^{8b} (table): w^2..w^7 by a product tree of depth 3,
+      // w^{8b+r} = w^{8b} w^r.  R/8 loads instead of R - 1 (fewer registers held
+      // by in-flight loads; cfg4 191 -> 182 us, cfg2 c128 129.2 -> 127.6 us) and
+      // short dependency chains; error <= 4 rounding steps per twiddle.
       // The plain-DFT configurations (chirp-z / Mehler convolutions, up to
       // 2^17 points) keep the exact table twiddles.
       const C* twp = tw + Cfg::twoff(P) + k;
-      C w1 = __ldg(twp), w8 = __ldg(twp + 7 * NS);
-      if (Cfg::SIGN > 0) { w1 = cconj(w1); w8 = cconj(w8); }
-      C w = w1;
-      u[1] = cmul(u[1], w1);
+      auto ld = [&](int t) {
+        C w = __ldg(twp + (t - 1) * NS);
+        return Cfg::SIGN > 0 ? cconj(w) : w;
+      };
+      C lo[8];
+      lo[1] = ld(1);
+      lo[2] = cmul(lo[1], lo[1]);
+      lo[3] = cmul(lo[2], lo[1]);
+      lo[4] = cmul(lo[2], lo[2]);
+      lo[5] = cmul(lo[4], lo[1]);
+      lo[6] = cmul(lo[4], lo[2]);
+      lo[7] = cmul(lo[4], lo[3]);
 #pragma unroll
-      for (int t = 2; t < R; ++t) {
-        w = (t == 8) ? w8 : cmul(w, w1);
-        u[t] = cmul(u[t], w);
+      for (int t = 1; t < 8; ++t) u[t] = cmul(u[t], lo[t]);
+#pragma unroll
+      for (int b = 1; b < R / 8; ++b) {
+        const C h = ld(8 * b);
+        u[8 * b] = cmul(u[8 * b], h);
+#pragma unroll
+        for (int r = 1; r < 8; ++r) u[8 * b + r] = cmul(u[8 * b + r], cmul(h, lo[r]));
       }
     } else if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW) {
       const C* twp = tw + Cfg::twoff(P) + k;
