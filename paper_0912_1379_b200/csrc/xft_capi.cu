@@ -2,6 +2,7 @@
 // validation, the host end-to-end pipeline, the transpose and the 2-D pass.
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <cstring>
@@ -119,7 +120,11 @@ int launch_pipe(const LaunchArgs& a) {
     occ = (o < 1 ? 1 : o) * sms;
   }
   const long long tiles = (a.batch + Cfg::ROWS - 1) / Cfg::ROWS;
-  const long long grid = tiles < occ ? tiles : occ;
+  long long cap = occ;
+#ifdef XFT_GRID_CAP_ENV  // tuning only: XFT_GRID_CAP=<ctas> caps the persistent grid
+  if (const char* e = getenv("XFT_GRID_CAP")) cap = atoll(e) < cap ? atoll(e) : cap;
+#endif
+  const long long grid = tiles < cap ? tiles : cap;
   RowConst kc;
   kc.half = a.tb.half;
   kc.cnabs = M_PI / std::sqrt(2.0 * double(1 << L));
