@@ -262,7 +262,43 @@ template <int SIGN, int K> __device__ __forceinline__ float2 w16odd(float2 a) {
   return p_fma(make_float2(-a.y, a.x), make_float2(s, s), p_mul(a, make_float2(c, c)));
 }
 
+#ifndef XFT_DFT16_44
+#define XFT_DFT16_44 1  // radix-16 butterfly as 4 x 4 (160 real ops) instead of 2 x 8 (168)
+#endif
+// 16-point DFT as 4 x 4: four 4-point DFTs down the columns n2 of x[4 n1 + n2],
+// the internal twiddles w16^(n2 k1), four 4-point DFTs along k1
+template <int SIGN, class C> __device__ __forceinline__ void dft16_44(C* v) {
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<SIGN>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+  // v[4 k1 + n2] now holds y[n2][k1]
+  v[4 + 1] = w16odd<SIGN, 1>(v[4 + 1]);    // k1=1 n2=1: w^1
+  v[4 + 2] = w8<SIGN, 1>(v[4 + 2]);        // k1=1 n2=2: w^2
+  v[4 + 3] = w16odd<SIGN, 3>(v[4 + 3]);    // k1=1 n2=3: w^3
+  v[8 + 1] = w8<SIGN, 1>(v[8 + 1]);        // k1=2 n2=1: w^2
+  v[8 + 2] = w8<SIGN, 2>(v[8 + 2]);        // k1=2 n2=2: w^4
+  v[8 + 3] = w8<SIGN, 3>(v[8 + 3]);        // k1=2 n2=3: w^6
+  v[12 + 1] = w16odd<SIGN, 3>(v[12 + 1]);  // k1=3 n2=1: w^3
+  v[12 + 2] = w8<SIGN, 3>(v[12 + 2]);      // k1=3 n2=2: w^6
+  {
+    const C t = w16odd<SIGN, 1>(v[12 + 3]);  // k1=3 n2=3: w^9 = -w^1
+    v[12 + 3] = mk(-t.x, -t.y);
+  }
+  C r[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    C a = v[4 * k1], b = v[4 * k1 + 1], c = v[4 * k1 + 2], d = v[4 * k1 + 3];
+    dft4<SIGN>(a, b, c, d);
+    r[k1] = a; r[k1 + 4] = b; r[k1 + 8] = c; r[k1 + 12] = d;  // X[k1 + 4 k2]
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = r[i];
+}
+
 template <int SIGN, class C> __device__ __forceinline__ void dft16(C* v) {
+  if constexpr (XFT_DFT16_44) {
+    dft16_44<SIGN>(v);
+    return;
+  }
   C e[8], o[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
