@@ -45,6 +45,9 @@
 #endif
 #include "xft_tma.cuh"
 
+#ifndef XFT_MIRROR
+#define XFT_MIRROR 1  // mirror lane map + shared rounding corrections (see PipeCfg::MIRROR)
+#endif
 #ifndef XFT_SPLIT
 #define XFT_SPLIT 1  // split next-row prefetch for single-row CTAs (see PipeCfg::SPLIT)
 #endif
@@ -381,6 +384,11 @@ struct PipeCfg {
   static constexpr int SPLIT0 = (SPLITOK_ && ROWS == 1 && STAGES == 1 && MINB_ == 1 && XFT_SPLIT && SMEM_MAX > MAIN)
                                     ? int((SMEM_MAX - MAIN) / sizeof(C)) / TR * TR : 0;
   static constexpr int SPLIT = SPLIT0 < N ? SPLIT0 : 0;
+  // Mirror lane map (row kernels, c128 LCT): lanes l and l^16 of a warp hold the
+  // columns j and TR-1-j, whose elements k and n-1-k share x^2 (x_{n-1-k} =
+  // -x_k exactly), hence the chirp-argument rounding corrections: each lane
+  // computes 8 of its 16 and takes the other 8 from its partner by shuffle.
+  static constexpr bool MIRROR = SPLITOK_ && C128 && MODE == MODE_LCT && TR % 32 == 0 && XFT_MIRROR;
   static constexpr size_t SMEM = MAIN + size_t(SPLIT) * sizeof(C);
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
@@ -668,11 +676,24 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], Load&& l
           } else {
             const double c2 = -2.0 * cin;
             const double o = opaque(tc.off0);  // per tile: keeps the 16 m's from being hoisted (and spilled)
+            if constexpr (Cfg::MIRROR) {
+              double e[E];
 #pragma unroll
-            for (int s = 0; s < E; ++s) {
-              const double eps = pre_eps(o + (double)(2 * s * TR), half, cin, c2);
-              v[s] = cmul(rot_eps(w.W, eps), ld(s));
-              if (s < E - 1) w.step(S, s < E - 2);
+              for (int s = 0; s < E / 2; ++s) e[s] = pre_eps(o + (double)(2 * s * TR), half, cin, c2);
+#pragma unroll
+              for (int s = E / 2; s < E; ++s) e[s] = __shfl_xor_sync(0xffffffffu, e[E - 1 - s], 16);
+#pragma unroll
+              for (int s = 0; s < E; ++s) {
+                v[s] = cmul(rot_eps(w.W, e[s]), ld(s));
+                if (s < E - 1) w.step(S, s < E - 2);
+              }
+            } else {
+#pragma unroll
+              for (int s = 0; s < E; ++s) {
+                const double eps = pre_eps(o + (double)(2 * s * TR), half, cin, c2);
+                v[s] = cmul(rot_eps(w.W, eps), ld(s));
+                if (s < E - 1) w.step(S, s < E - 2);
+              }
             }
           }
         } else if (mode == 3) {
@@ -762,11 +783,24 @@ __device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, 
         } else {
           const double c2 = -2.0 * cout;
           const double o = opaque(tc.off0);
+          if constexpr (Cfg::MIRROR) {  // y_{n-1-k} = -y_k exactly: the corrections are shared too
+            double e[E];
 #pragma unroll
-          for (int s = 0; s < E; ++s) {
-            const double eps = post_eps(o + (double)(2 * s * TR), half, s4, cout, c2);
-            emit(s, cmul(rot_eps(w.W, eps), v[s]));
-            if (s < E - 1) w.step(S, s < E - 2);
+            for (int s = 0; s < E / 2; ++s) e[s] = post_eps(o + (double)(2 * s * TR), half, s4, cout, c2);
+#pragma unroll
+            for (int s = E / 2; s < E; ++s) e[s] = __shfl_xor_sync(0xffffffffu, e[E - 1 - s], 16);
+#pragma unroll
+            for (int s = 0; s < E; ++s) {
+              emit(s, cmul(rot_eps(w.W, e[s]), v[s]));
+              if (s < E - 1) w.step(S, s < E - 2);
+            }
+          } else {
+#pragma unroll
+            for (int s = 0; s < E; ++s) {
+              const double eps = post_eps(o + (double)(2 * s * TR), half, s4, cout, c2);
+              emit(s, cmul(rot_eps(w.W, eps), v[s]));
+              if (s < E - 1) w.step(S, s < E - 2);
+            }
           }
         }
       } else if (rcs.post == 3) {
@@ -836,7 +870,9 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
 
   const int tid = threadIdx.x;
   const int lrow = tid / Cfg::TR;
-  const int j = tid - lrow * Cfg::TR;
+  const int jt = tid - lrow * Cfg::TR;
+  const int j = Cfg::MIRROR ? ((jt & 16) ? Cfg::TR - 1 - (((jt >> 5) << 4) | (jt & 15)) : (((jt >> 5) << 4) | (jt & 15)))
+                            : jt;
   const long long ntiles = (batch + ROWS - 1) / ROWS;
   const long long G = gridDim.x;
   const ThreadConst<Cfg> tc(j);
