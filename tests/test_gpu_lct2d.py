@@ -108,3 +108,26 @@ def test_columns_tall(torch, L2, R, dtype, tol, inplace):
         assert np.all(got[:, nc:] == 0)  # columns outside the slab untouched
     else:
         assert np.array_equal(got[:, nc:], full[:, nc:])
+
+
+@pytest.mark.parametrize("n,dtype,tol", [(2048, np.complex64, 1e-6), (512, np.complex128, 1e-13)])
+def test_sharded_over_nccl_world1(torch, L2, tmp_path, n, dtype, tol):
+    """lct2d_sharded through a real NCCL process group (one rank: the only GPU of this box):
+    packed row pass -> ncclAllToAll (all_to_all_single) -> column pass on the received slab."""
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        pytest.skip("a process group is already active")
+    store = dist.FileStore(str(tmp_path / "store"), 1)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(17)
+        f = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(dtype)
+        ft = torch.from_numpy(f).cuda()
+        got = L2.lct2d_sharded(ft, ABCD5, (0.5, 1.5, -0.5, 0.5))
+        torch.cuda.synchronize()
+        ref = L2.lct2d(ft, ABCD5, (0.5, 1.5, -0.5, 0.5))
+        assert got.shape == (n, n)
+        assert rel_l2(got.cpu().numpy(), ref.cpu().numpy()) <= tol
+    finally:
+        dist.destroy_process_group()
