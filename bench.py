@@ -294,10 +294,11 @@ def run_ours(args, rank, world, local_rank):
             L2.lct2d_sharded(st.vin, st.p, st.p, buffers=st.bufs)
 
     sets = [[make_state(it) for it in work] for _ in range(nsets)]
-    # Mehler plans upload per-row tables from the host and the sharded 2-D pass calls
-    # NCCL through torch.distributed: those steps are launched directly; everything
-    # else is captured as CUDA graphs so the timed loop has no Python launch overhead.
-    capturable = all(it.kind == "lct" or (it.kind == "lct2d" and world == 1) for it in work)
+    # The sharded 2-D pass calls NCCL through torch.distributed: it is launched
+    # directly; everything else (incl. the Mehler path, whose per-row plans are
+    # built and cached on the device by the warm-up call before capture) is
+    # captured as CUDA graphs so the timed loop has no host launch overhead.
+    capturable = all(it.kind in ("lct", "mehler") or (it.kind == "lct2d" and world == 1) for it in work)
     chunk = max(1, min(10, args.steps))
 
     def runner(item_idx):
