@@ -36,12 +36,14 @@ void host_fft(std::vector<cld>& a, int s) {
     j ^= bit;
     if (i < j) std::swap(a[i], a[j]);
   }
+  std::vector<cld> w;
   for (size_t len = 2; len <= n; len <<= 1) {
     const long double ang = s * 2.0L * PI_L / (long double)len;
+    w.resize(len / 2);
+    for (size_t k = 0; k < len / 2; ++k) w[k] = cld(cosl(ang * k), sinl(ang * k));  // once per stage
     for (size_t i = 0; i < n; i += len)
       for (size_t k = 0; k < len / 2; ++k) {
-        const cld w(cosl(ang * k), sinl(ang * k));
-        const cld u = a[i + k], v = a[i + k + len / 2] * w;
+        const cld u = a[i + k], v = a[i + k + len / 2] * w[k];
         a[i + k] = u + v;
         a[i + k + len / 2] = u - v;
       }
@@ -169,10 +171,12 @@ int run_chirpz(int mode, int sign, const void* in, void* out, int64_t batch, int
   if (n < 2) return XFT_EINVALID_SIZE;
   int64_t m = 1;
   while (m < 2 * n - 1) m *= 2;
-  if (m > chirpz_max_m(dtype)) return XFT_ENOTSUP;
   CzPlan p;
   int rc = get_plan(n, mode == 0 ? sign : -1, mode == 0 ? 0 : 1, &p);
   if (rc) return rc;
+  if (m > chirpz_max_m(dtype))  // beyond one CTA: the four-step convolution
+    return run_large_chirpz(mode == 2, (flags & XFT_FLAG_BARE_FOURIER) ? 1 : 0, in, out, batch, n, dtype, abcd, stride,
+                            uni4, p.pre, p.post, p.hspec, m, st);
   OpChirpZ op;
   op.pre = p.pre;
   op.post = p.post;

@@ -18,6 +18,12 @@ int64_t chirpz_max_m(int dtype);
 // four-step path (xft_large.cu) for rows longer than the in-CTA kernels
 int run_large_pow2(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype,
                    const double* abcd, int64_t stride, const double* uni4, int flags, cudaStream_t st);
+// chirp-z route beyond the in-CTA sizes (xft_large.cu): the same convolution as
+// run_chirpz (pre/post multipliers and the natural-order filter spectrum of
+// its plan, convolution length m = 2^l) through the four-step tile passes
+int run_large_chirpz(int lct, int bare, const void* in, void* out, int64_t batch, int64_t n, int dtype,
+                     const double* abcd, int64_t stride, const double* uni4, const void* pre, const void* post,
+                     const void* hspec, int64_t m, cudaStream_t st);
 struct OpMehlerRow;
 int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm, int l,
                      int64_t n, cudaStream_t st);

@@ -550,6 +550,70 @@ int run_large_pow2(int mode, int sign, const void* in, void* out, int64_t batch,
                           : large_pow2<double2>(mode, sign, in, out, batch, n, abcd, stride, uni, flags, st);
 }
 
+// chirp-z rows whose convolution length m exceeds the in-CTA kernels:
+// u = pre x f [x e^{i phi}] zero-padded to m -> columns pass -> rows pass
+// (forward, x filter spectrum, inverse) -> inverse columns with the post
+// multiplier (xft/fftcore.py:84-100, 116-119; the LCT wrappers of
+// xft/lct.py:204-207).  The filter spectrum is permuted once into the
+// four-step order [k1][k2] = H[k1 + M1 k2] and cached per (plan, dtype).
+template <class C>
+__global__ void permute_spectrum_kernel(C* out, const double2* hnat, int M1, int M2) {
+  const long long M = (long long)M1 * M2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (long long)gridDim.x * blockDim.x) {
+    const long long k1 = i / M2, k2 = i - k1 * M2;
+    out[i] = to_c<C>(hnat[k1 + (long long)M1 * k2]);
+  }
+}
+
+std::mutex g_czmu;
+std::map<std::tuple<int, const void*, int>, void*> g_czperm;  // (device, plan spectrum, dtype)
+
+template <class C>
+int large_chirpz(int lct, int bare, const C* in, C* out, int64_t batch, int64_t n, const double* abcd, int64_t stride,
+                 Abcd uni, const double2* pre, const double2* post, const double2* hspec, int64_t m, cudaStream_t st) {
+  constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
+  constexpr int W = tile_w<C>();
+  const int l = log2_of(m);
+  const Shape sh = split(l);
+  if (sh.l1 < LMIN || sh.l1 > LMAX || sh.l2 < LMIN || sh.l2 > LMAX) return XFT_ENOTSUP;
+  const int M1 = 1 << sh.l1, M2 = 1 << sh.l2;
+  const void* twm = nullptr;
+  int rc = natural_twiddles(sh.M, dtype, &twm);
+  if (rc) return rc;
+  C* spec = nullptr;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_czmu);
+    auto key = std::make_tuple(dev, (const void*)hspec, dtype);
+    auto it = g_czperm.find(key);
+    if (it == g_czperm.end()) {
+      void* d = nullptr;
+      if (cudaMalloc(&d, sh.M * sizeof(C)) != cudaSuccess) return XFT_ECUDA;
+      permute_spectrum_kernel<C><<<592, 256>>>(static_cast<C*>(d), hspec, M1, M2);  // legacy stream: before any use
+      if (cudaDeviceSynchronize() != cudaSuccess) return XFT_ECUDA;
+      it = g_czperm.emplace(key, d).first;
+    }
+    spec = static_cast<C*>(it->second);
+  }
+  DevBuf<C> scr(st);
+  DevBuf<RowChirp> rcs(st);
+  if ((rc = scr.alloc((size_t)batch * sh.M))) return rc;
+  if (lct) {
+    if ((rc = rcs.alloc(batch))) return rc;
+    row_chirp_kernel<<<(unsigned)((batch + 127) / 128), 128, 0, st>>>(rcs.p, batch, abcd, stride, uni, bare);
+  }
+  const long long t1 = batch * (M2 / W), t2 = batch * (M1 / W);
+  const double half = host_half_step(n);
+  OpCols<C, GenChirpZ<C>> c1{GenChirpZ<C>{in, rcs.p, pre, half, n, lct}, scr.p, static_cast<const C*>(twm), M2, W,
+                             sh.M, 0};
+  if ((rc = tile<C, true, true, -1>(sh.l1, t1, c1, st))) return rc;
+  OpRowsConv<C> c2{scr.p, spec, 0, static_cast<const C*>(twm), M1, M2, W, sh.M};
+  if ((rc = tile<C, false, false, -1>(sh.l2, t2, c2, st))) return rc;
+  OpColsInv<C, PostChirpZ<C>> c3{scr.p, PostChirpZ<C>{out, rcs.p, post, half, n, lct}, M2, W, sh.M};
+  return tile<C, true, true, +1>(sh.l1, t1, c3, st);
+}
+
 // Mehler rows whose window needs M > in-CTA limit (complex128)
 int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm,
                      int l, int64_t n, cudaStream_t st) {
@@ -579,6 +643,20 @@ int run_large_mehler(const void* in, void* out, long long rows, const int* rowli
   if ((rc = tile<C, true, true, +1>(sh.l1, t1, u3, st))) return rc;
   mehler_zero_kernel<<<(unsigned)rows, 256, 0, st>>>(static_cast<C*>(out), rowlist, prm, n);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+int run_large_chirpz(int lct, int bare, const void* in, void* out, int64_t batch, int64_t n, int dtype,
+                     const double* abcd, int64_t stride, const double* uni4, const void* pre, const void* post,
+                     const void* hspec, int64_t m, cudaStream_t st) {
+  const Abcd uni = uni4 ? Abcd{uni4[0], uni4[1], uni4[2], uni4[3]} : Abcd{0, 0, 0, 0};
+  const auto* p = static_cast<const double2*>(pre);
+  const auto* q = static_cast<const double2*>(post);
+  const auto* h = static_cast<const double2*>(hspec);
+  return dtype == XFT_C64
+             ? large_chirpz<float2>(lct, bare, static_cast<const float2*>(in), static_cast<float2*>(out), batch, n,
+                                    abcd, stride, uni, p, q, h, m, st)
+             : large_chirpz<double2>(lct, bare, static_cast<const double2*>(in), static_cast<double2*>(out), batch,
+                                     n, abcd, stride, uni, p, q, h, m, st);
 }
 
 }  // namespace xftb

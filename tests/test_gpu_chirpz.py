@@ -177,3 +177,41 @@ def test_mehler_config3_full(torch, X):
     for r in range(z.shape[0]):
         ideal = math.sqrt(2 * math.pi) * z[r] ** c3.extra["m"][r] * psi[r]
         assert np.linalg.norm(g_psi[r] - ideal) <= 1e-6 * max(np.linalg.norm(ideal), 1e-9), r
+
+
+# ---- rows beyond the in-CTA sizes: four-step convolution (non-powers of two)
+# and four-step row transforms (powers of two) -------------------------------
+LARGE_NONPOW2 = [(5000, np.complex128), (12000, np.complex64), (196608, np.complex128), (196608, np.complex64)]
+
+
+@pytest.mark.parametrize("n,dtype", LARGE_NONPOW2)
+def test_chirpz_large_lct_dft_scaled(torch, X, n, dtype):
+    """Chirp-z rows whose convolution length exceeds one CTA (196608 = the reference CLI bench size,
+    pkg/tests/test_cli.py:216-220): LCT, both DFT signs and the scaled Fourier against the oracle."""
+    tol = 1e-12 if dtype == np.complex128 else 2e-5
+    rng = np.random.default_rng(n)
+    rows = 2
+    f = ((rng.standard_normal((rows, n)) + 1j * rng.standard_normal((rows, n))) / math.sqrt(2)).astype(dtype)
+    al = np.array([0.7, 2.2])
+    abcd = np.stack([np.cos(al), np.sin(al), -np.sin(al), np.cos(al)], 1)
+    fd = dev(torch, f)
+    got = X.ops.lct_rows(fd, abcd).cpu().numpy()
+    _, ref = O.fast_lct_rows(abcd, f.astype(complex))
+    assert max_row_rel_l2(got, ref) <= tol
+    for sign in (-1, 1):
+        got = X.ops.dft_rows(fd, sign).cpu().numpy()
+        assert max_row_rel_l2(got, O.dft_rows(f.astype(complex), sign)) <= tol
+    got = X.ops.scaled_fourier_rows(fd).cpu().numpy()
+    assert max_row_rel_l2(got, O.scaled_fourier_rows(f.astype(complex))) <= tol
+
+
+@pytest.mark.parametrize("n,dtype", [(65536, np.complex128), (1 << 20, np.complex128), (1 << 20, np.complex64)])
+def test_large_pow2_lct(torch, X, n, dtype):
+    """Power-of-two rows up to xft_max_n (2^20) through the four-step row path."""
+    tol = 1e-12 if dtype == np.complex128 else 2e-5
+    rng = np.random.default_rng(n + 1)
+    f = ((rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))) / math.sqrt(2)).astype(dtype)
+    abcd = np.array([[2.0, 1.0, 1.0, 1.0], [math.cos(1.1), math.sin(1.1), -math.sin(1.1), math.cos(1.1)]])
+    got = X.ops.lct_rows(dev(torch, f), abcd).cpu().numpy()
+    _, ref = O.fast_lct_rows(abcd, f.astype(complex))
+    assert max_row_rel_l2(got, ref) <= tol
