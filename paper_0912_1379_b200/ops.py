@@ -177,9 +177,23 @@ def lct_chain_rows(values, stages, *, scale=1.0, reverse=False, out=None):
     p = np.ascontiguousarray(np.asarray(stages, dtype=np.float64).reshape(-1, 4))
     if out is None:
         out = torch.empty_like(v)
-    with torch.cuda.device(v.device):
-        _native.call("xft_lct_chain", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v), p.ctypes.data,
-                     p.shape[0], float(scale), int(bool(reverse)), _stream_ptr(v.device))
+    if B == 0:
+        return out
+    if not 1 <= p.shape[0] <= 4:
+        raise ParameterError(f"a chain holds 1 to 4 stages (got {p.shape[0]})")
+    if n & (n - 1) == 0 and 32 <= n <= (16384 if v.dtype == torch.complex64 else 8192):
+        with torch.cuda.device(v.device):
+            _native.call("xft_lct_chain", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v), p.ctypes.data,
+                         p.shape[0], float(scale), int(bool(reverse)), _stream_ptr(v.device))
+        return out
+    # rows the one-launch chain does not hold on chip (non-powers of two, long or
+    # short rows): the stages one after another through the row kernels
+    cur = v
+    for st in p:
+        cur = lct_rows(cur, tuple(float(t) for t in st))
+    if reverse:
+        cur = cur.flip(1)
+    out.copy_(cur * scale if scale != 1.0 else cur)
     return out
 
 

@@ -158,3 +158,18 @@ def test_b_zero_batched_per_row(torch, X, dtype):
     bad[4, 0] = 1.0 / bad[4, 3]
     with pytest.raises(X.errors.UnsupportedBranchError):
         X.ops.lct_b_zero_rows(torch.from_numpy(s).cuda(), bad)
+
+
+@pytest.mark.parametrize("n,dtype", [(1000, "c128"), (16, "c64"), (65536, "c128")])
+def test_chain_sizes_beyond_one_launch(torch, X, n, dtype):
+    """Rows the one-launch chain kernel does not hold (non-powers of two, short, long): staged through the
+    row kernels, same semantics (scale, reverse) as the fused chain."""
+    rng = np.random.default_rng(n)
+    f = _signal(rng, 2, n).astype(np.complex64 if dtype == "c64" else np.complex128)
+    got = X.ops.inverse_roundtrip_rows(torch.from_numpy(f).cuda(), (2.0, 1.0, 1.0, 1.0)).cpu().numpy()
+    a, b, c, d = 2.0, 1.0, 1.0, 1.0
+    sigma = 4.0 * b / np.pi
+    ref = O.fast_lct_rows((a, b, c, d), f.astype(np.complex128))[1]
+    ref = O.fast_lct_rows((d * sigma, -b / sigma, -c * sigma, a / sigma), ref)[1][:, ::-1] * np.sqrt(sigma)
+    err = max_row_rel_l2(got.astype(np.complex128), ref)
+    assert err <= (TOL128 if dtype == "c128" else TOL64), err
