@@ -163,6 +163,9 @@ __device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd
 #ifndef XFT_C128_WALK
 #define XFT_C128_WALK 1  // 0: every c128 chirp through the per-element table path (modes 3/4)
 #endif
+#ifndef XFT_WALK_SMOOTH_BELOW
+#define XFT_WALK_SMOOTH_BELOW 2048.0  // rows with max |phase| below this skip the rounding corrections
+#endif
 struct DD {
   double hi, lo;
 };
@@ -248,7 +251,7 @@ __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abc
   const double y2 = fabs(c.s4) * x2;
   const double pmax_out = fabs(c.cout) * y2 * y2;
   auto mode_of = [](double pm) {
-    if (XFT_C128_WALK && pm < 2048.0) return 1;
+    if (XFT_C128_WALK && pm < XFT_WALK_SMOOTH_BELOW) return 1;
     if (XFT_C128_WALK && pm < 16777216.0) return 2;
     return pm < 1e12 ? 3 : 4;
   };
