@@ -55,7 +55,10 @@ extern "C" {
 /* Library version (major*10000 + minor*100 + patch). */
 int xft_version(void);
 
-/* Largest power-of-two row length the single-kernel path accepts for dtype. */
+/* Largest power-of-two row length the row entry points accept for dtype
+ * (2^20: in-CTA kernels up to 2^14 c64 / 2^13 c128, four-step tile passes
+ * beyond).  Other lengths take the chirp-z route (xft/fftcore.py:84-100) up to
+ * a convolution length of 2^20, i.e. n <= 524288. */
 int64_t xft_max_n(int dtype);
 
 /* Build (once) the immutable tables for (current device, n, dtype).  Must be
