@@ -284,14 +284,21 @@ def run_ours(args, rank, world, local_rank):
         return st
 
     def launch(it, st):
+        """Launches one transform; returns the tensor holding its result."""
         if it.kind == "lct":
-            ops.lct_rows(st.vin, st.p, out=st.vout, validate=False)
+            return ops.lct_rows(st.vin, st.p, out=st.vout, validate=False)
         elif it.kind == "mehler":
-            mehler.mehler_rows(st.vin, st.p, out=st.vout)
+            return mehler.mehler_rows(st.vin, st.p, out=st.vout)
         elif world == 1:
-            L2.lct2d(st.vin, st.p, st.p, out=st.vout, workspace=st.ws)
+            return L2.lct2d(st.vin, st.p, st.p, out=st.vout, workspace=st.ws)
         else:
-            L2.lct2d_sharded(st.vin, st.p, st.p, buffers=st.bufs)
+            if args.transport == "p2p":
+                try:  # row kernel stores straight into the peers' symmetric-memory slabs
+                    return L2.lct2d_sharded(st.vin, st.p, st.p, transport="p2p")
+                except (RuntimeError, NotImplementedError) as e:
+                    print(f"p2p transport unavailable ({e}); falling back to NCCL all_to_all", file=sys.stderr)
+                    args.transport = "nccl"
+            return L2.lct2d_sharded(st.vin, st.p, st.p, buffers=st.bufs)
 
     sets = [[make_state(it) for it in work] for _ in range(nsets)]
     # The sharded 2-D pass calls NCCL through torch.distributed: it is launched
@@ -388,8 +395,7 @@ def run_ours(args, rank, world, local_rank):
                 st = sets[0][work.index(it)]
                 st.vin.copy_(hin, non_blocking=True)
                 with torch.cuda.stream(torch.cuda.current_stream(dev)):
-                    launch(it, st)
-                res = st.vout if it.kind != "lct2d" or world == 1 else st.bufs[1]
+                    res = launch(it, st)
                 hout.view(-1)[:res.numel()].copy_(res.view(-1), non_blocking=True)
                 torch.cuda.current_stream(dev).synchronize()
 
@@ -454,7 +460,9 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded, BASELINE config draw order)",
         "config": dict(cfg, l2="3 rotating input/output sets; each launch streams >= 2x L2 of cold data",
                        parallelism=(f"batch-sharded x{world}, no collective" if args.config != "cfg5"
-                                    else f"row-sharded x{world}, one NCCL all_to_all_single"),
+                                    else f"row-sharded x{world}, " + ("row-kernel NVLink peer stores (symmetric memory)"
+                                                                     if args.transport == "p2p" and world > 1
+                                                                     else "one NCCL all_to_all_single")),
                        timing="CUDA graphs" if capturable else "direct launches"),
         "roofline": roof, "per_dtype": per, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "Msamples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -477,6 +485,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=None, help="CPU baseline rows per item (default: full batch)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="cfg5 under torchrun: row-kernel NVLink peer stores (p2p) or NCCL all_to_all")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -138,6 +138,16 @@ int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, i
 int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd_host,
                         int seg_log2w, int64_t seg_stride, void* stream);
 
+/* Row LCT (one quadruple, host) whose epilogue stores segment h (n/npeers
+ * samples) of local row r straight into peer buffer h at row row0 + r, i.e.
+ * peer_ptrs[h] + (row0 + r) * n/npeers: the all-to-all of the sharded 2-D
+ * transform done by the row kernel's own stores over NVLink (peer_ptrs: device
+ * addresses valid in this process, e.g. symmetric-memory / IPC mappings; host
+ * array of npeers <= 8).  The caller synchronises the ranks before reading the
+ * peer buffers.  n a power of two, 32 <= n <= in-CTA limit, npeers | n. */
+int xft_lct_rows_peers(const void* in, const uint64_t* peer_ptrs, int npeers, int64_t row0, int64_t batch, int64_t n,
+                       int dtype, const double* abcd_host, void* stream);
+
 /* Composed transform in one launch (device in/out, parameters on the host):
  * out = scale * R(L_{nst} ... L_2 L_1 in), 1 <= nst <= 4, each stage reading the
  * previous stage's output as samples on the standard grid; R reverses the

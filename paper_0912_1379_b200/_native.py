@@ -49,6 +49,7 @@ _SIGS = {
     "xft_transpose": ([_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
     "xft_lct_columns": ([_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
     "xft_lct_rows_packed": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, ctypes.c_int, _i64, _vp], ctypes.c_int),
+    "xft_lct_rows_peers": ([_vp, _vp, ctypes.c_int, _i64, _i64, _i64, ctypes.c_int, _vp, _vp], ctypes.c_int),
     "xft_lct_chain": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, _vp],
                       ctypes.c_int),
     "xft_lct_b_zero": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, _vp], ctypes.c_int),

@@ -32,6 +32,7 @@ struct LaunchArgs {
   cudaStream_t st;
   int seg_log2w = 0;        // segmented (all-to-all send) output layout
   long long seg_stride = 0;  // 0: natural rows
+  PeerTable peers{};         // peer-store output (count > 0)
 };
 
 using LaunchFn = int (*)(const LaunchArgs&);
@@ -134,7 +135,7 @@ int launch_pipe(const LaunchArgs& a) {
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
       static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
       static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc, a.seg_log2w,
-      a.seg_stride);
+      a.seg_stride, a.peers);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
 }
 
@@ -166,7 +167,7 @@ int log2_exact(int64_t n) {
 
 int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype,
              const double* abcd, int64_t stride, Abcd uni, int flags, cudaStream_t st, int seg_log2w = 0,
-             long long seg_stride = 0) {
+             long long seg_stride = 0, const PeerTable* peers = nullptr) {
   if (n < 1) return XFT_EINVALID_SIZE;
   if (batch < 0) return XFT_EINVALID_SIZE;
   if (dtype != XFT_C64 && dtype != XFT_C128) return XFT_EPARAM;
@@ -180,10 +181,17 @@ int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64
     const double u4[4] = {uni.a, uni.b, uni.c, uni.d};
     return run_large_pow2(mode, sign, in, out, batch, n, dtype, abcd, stride, u4, flags, st);
   }
+  if ((seg_stride || peers) && (1 << l) <= pipe_radix(dtype, l))
+    return XFT_ENOTSUP;  // segmented / peer epilogues live in the pipelined row kernel
   LaunchArgs a{in, out, (long long)batch, abcd, (long long)stride, uni, {}, flags, st};
   a.seg_log2w = seg_log2w;
   a.seg_stride = seg_stride;
   if (seg_stride && (seg_log2w < 0 || seg_log2w > l || mode != MODE_LCT)) return XFT_EPARAM;
+  if (peers) {
+    if (mode != MODE_LCT || peers->count < 1 || peers->count > 8 || (int64_t(peers->count) << seg_log2w) != n)
+      return XFT_EPARAM;
+    a.peers = *peers;
+  }
   int rc = get_tables(n, dtype, &a.tb);
   if (rc) return rc;
   LaunchFn fn = nullptr;
@@ -388,6 +396,26 @@ int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int
   const Abcd u{abcd_host[0], abcd_host[1], abcd_host[2], abcd_host[3]};
   return run_rows(MODE_LCT, -1, in, out, batch, n, dtype, nullptr, 0, u, 0, static_cast<cudaStream_t>(stream),
                   seg_log2w, seg_stride);
+}
+
+int xft_lct_rows_peers(const void* in, const uint64_t* peer_ptrs, int npeers, int64_t row0, int64_t batch, int64_t n,
+                       int dtype, const double* abcd_host, void* stream) {
+  int rc = xft_validate_lct_params(abcd_host, 1, 0, 1, 1e-10, nullptr);
+  if (rc) return rc;
+  if (npeers < 1 || npeers > 8 || n % npeers || row0 < 0) return XFT_ESHAPE;
+  const int64_t nc = n / npeers;
+  const int segl = log2_exact(nc);
+  if (segl < 0) return XFT_ESHAPE;
+  const int l = log2_exact(n);
+  if (l < 0 || l > (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128) || (1 << l) <= pipe_radix(dtype, l))
+    return XFT_ENOTSUP;  // the peer epilogue lives in the pipelined row kernel
+  PeerTable pt{};
+  for (int h = 0; h < npeers; ++h) pt.p[h] = reinterpret_cast<void*>(static_cast<uintptr_t>(peer_ptrs[h]));
+  pt.row0 = row0;
+  pt.count = npeers;
+  const Abcd u{abcd_host[0], abcd_host[1], abcd_host[2], abcd_host[3]};
+  return run_rows(MODE_LCT, -1, in, nullptr, batch, n, dtype, nullptr, 0, u, 0, static_cast<cudaStream_t>(stream),
+                  segl, 0, &pt);
 }
 
 int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,

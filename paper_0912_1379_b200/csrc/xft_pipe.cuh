@@ -732,13 +732,25 @@ __device__ __forceinline__ void pre_multiply(typename Cfg::C (&v)[Cfg::E], const
 // the sharded 2-D transform: segment g of row r lands at g*seg_stride + r*2^segl)
 template <class C>
 struct OutRow {
-  C* base;  // natural: row start; segmented: out + r * 2^segl
+  C* base;  // natural: row start; segmented: out + r * 2^segl; peer: (row0 + r) * 2^segl
   long long seg_stride;
   int segl;
+  void* const* peers;  // peer mode (seg_stride < 0): segment h goes to peers[h] + base offset
   __device__ __forceinline__ C* at(int c) const {
     if (seg_stride == 0) return base + c;
+    if (seg_stride < 0)
+      return static_cast<C*>(peers[c >> segl]) + reinterpret_cast<long long>(base) + (c & ((1 << segl) - 1));
     return base + (long long)(c >> segl) * seg_stride + (c & ((1 << segl) - 1));
   }
+};
+
+// Peer destinations of the sharded 2-D transform's row pass: segment h of
+// every row is stored straight into rank h's receive slab (NVLink peer
+// memory), at row row0 + r, so the all-to-all is the row kernel's own stores.
+struct PeerTable {
+  void* p[8];
+  long long row0;
+  int count;  // 0: not used
 };
 
 // post-multiplier of element s of a thread's E registers, handed to emit(s, value)
@@ -855,7 +867,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restrict__ out, long long batch,
                 const double* __restrict__ abcd, long long abcd_stride, Abcd uni, const typename Cfg::C* __restrict__ tw,
                 const typename Cfg::C* __restrict__ ptab, const void* __restrict__ gtab, double2 cn, RowConst kc,
-                int seg_log2w, long long seg_stride) {
+                int seg_log2w, long long seg_stride, const __grid_constant__ PeerTable peers) {
   using C = typename Cfg::C;
   using Coef = typename Cfg::Coef;
   constexpr int N = Cfg::N, ROWS = Cfg::ROWS, S = Cfg::STAGES;
@@ -1009,8 +1021,11 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
         for (int s = 0; s < Cfg::E; ++s) st_stream(out + row * N + j + s * Cfg::TR, v[s]);
     } else {
       if (row < batch) {
-        const OutRow<C> o{seg_stride ? out + (row << seg_log2w) : out + (XFT_NOMEM ? (long long)blockIdx.x * ROWS + lrow : row) * N, seg_stride,
-                          seg_log2w};
+        const OutRow<C> o{
+            peers.count ? reinterpret_cast<C*>((peers.row0 + row) << seg_log2w)
+            : seg_stride ? out + (row << seg_log2w)
+                         : out + (XFT_NOMEM ? (long long)blockIdx.x * ROWS + lrow : row) * N,
+            peers.count ? -1 : seg_stride, seg_log2w, peers.p};
         post_store<Cfg>(v, o, j, rc, tc, kc, cn, ptab, tab);
       }
     }

@@ -63,6 +63,26 @@ def rows_packed(local, abcd_row, world: int, out=None):
     return out
 
 
+def rows_to_peers(local, abcd_row, peer_ptrs, row0: int):
+    """Row LCT of the local [rl, n] rows whose epilogue stores segment h of row r
+    straight into peer slab h ([n, n/G] row-major, device pointer peer_ptrs[h]) at
+    row row0 + r: the all-to-all of the sharded transform done by the row kernel's
+    own NVLink stores (``xft_lct_rows_peers``).  The caller synchronises the ranks
+    before the column pass reads its slab."""
+    import ctypes
+
+    rl, n = local.shape
+    G = len(peer_ptrs)
+    if not 1 <= G <= 8 or n % G:
+        raise ShapeError(f"{G} peers do not split n = {n}")
+    ptrs = (ctypes.c_uint64 * G)(*[int(p) for p in peer_ptrs])
+    p = _abcd4(abcd_row)
+    torch = ops._torch()
+    with torch.cuda.device(local.device):
+        _native.call("xft_lct_rows_peers", local.data_ptr(), ctypes.addressof(ptrs), G, int(row0), rl, n,
+                     ops._dtype_code(local), p.ctypes.data, ops._stream_ptr(local.device))
+
+
 def columns_inplace(slab, abcd_col, workspace=None):
     """Column LCT of a row-major [n, nc] slab, in place."""
     torch = ops._torch()
@@ -76,7 +96,23 @@ def columns_inplace(slab, abcd_col, workspace=None):
     return slab
 
 
-def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, col_fn=None, buffers=None):
+_P2P = {}  # (group, n, dtype, device) -> (symmetric receive slab, its rendezvous handle)
+
+
+def _p2p_slab(group, n, nc, dtype, device):
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+
+    key = (dist.get_group_rank(group, dist.get_rank()) if group is not None else dist.get_rank(),
+           id(group), n, dtype, str(device))
+    if key not in _P2P:
+        slab = symm.empty((n, nc), dtype=dtype, device=device)
+        _P2P[key] = (slab, symm.rendezvous(slab, group if group is not None else dist.group.WORLD))
+    return _P2P[key]
+
+
+def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, col_fn=None, buffers=None,
+                  transport="nccl"):
     """Sharded 2-D LCT over the ranks of ``group``.
 
     ``local``: this rank's [n/G, n] rows.  Returns this rank's [n, n/G] column
@@ -84,6 +120,13 @@ def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, co
     and ``col_fn(slab, abcd) -> slab`` default to the CUDA kernels; tests on
     CPU (gloo) substitute the CPU oracle to check the orchestration/layout.
     ``buffers``: optional preallocated (send, recv) of shape [world, rl, nc].
+
+    ``transport``: "nccl" -- packed row pass, ``all_to_all_single``, column pass;
+    "p2p" -- the row kernel stores every segment straight into the owning
+    rank's symmetric-memory receive slab over NVLink (no separate collective,
+    ``xft_lct_rows_peers``), two device-side barriers, column pass in place.
+    The p2p result is that persistent slab: the next p2p call of the same shape
+    overwrites it.
     """
     import torch
     import torch.distributed as dist
@@ -95,6 +138,15 @@ def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, co
     if rl * world != n:
         raise ShapeError(f"{world} ranks x {rl} rows do not tile an n = {n} field")
     nc = n // world
+    if transport == "p2p":
+        rank = dist.get_rank(group)
+        slab, hdl = _p2p_slab(group, n, nc, local.dtype, local.device)
+        hdl.barrier()  # every rank's slab is free (previous column pass done)
+        rows_to_peers(local, abcd_row, list(hdl.buffer_ptrs), rank * rl)
+        hdl.barrier()  # every rank's stores into this slab have landed
+        return (col_fn or columns_inplace)(slab, abcd_col)
+    if transport != "nccl":
+        raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
     row_fn = row_fn or (lambda x, p, w: rows_packed(x, p, w, out=None if buffers is None else buffers[0]))
     col_fn = col_fn or columns_inplace
     send = row_fn(local, abcd_row, world)

@@ -131,3 +131,45 @@ def test_sharded_over_nccl_world1(torch, L2, tmp_path, n, dtype, tol):
         assert rel_l2(got.cpu().numpy(), ref.cpu().numpy()) <= tol
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G,dtype,tol", [(4, np.complex64, 1e-6), (2, np.complex128, 1e-13), (8, np.complex64, 1e-6)])
+def test_peer_store_rows_emulate_shards(torch, L2, G, dtype, tol):
+    """xft_lct_rows_peers with G virtual ranks on one GPU: each 'rank' stores its row segments straight
+    into the G receive slabs (the NVLink peer-store all-to-all); the slabs then hold the column blocks."""
+    n = 1024
+    rng = np.random.default_rng(21)
+    f = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(dtype)
+    ft = torch.from_numpy(f).cuda()
+    rl, nc = n // G, n // G
+    slabs = [torch.full((n, nc), float("nan"), dtype=ft.dtype, device=ft.device) for _ in range(G)]
+    ptrs = [s.data_ptr() for s in slabs]
+    for g in range(G):
+        L2.rows_to_peers(ft[g * rl:(g + 1) * rl], ABCD5, ptrs, g * rl)
+    full = L2.lct2d(ft, ABCD5, ABCD5)
+    for h in range(G):
+        L2.columns_inplace(slabs[h], ABCD5)
+        assert rel_l2(slabs[h].cpu().numpy(), full[:, h * nc:(h + 1) * nc].cpu().numpy()) <= tol
+
+
+def test_sharded_p2p_symmetric_memory_world1(torch, L2, tmp_path):
+    """lct2d_sharded(transport="p2p") through torch symmetric memory (one rank on this box's one GPU)."""
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        pytest.skip("a process group is already active")
+    store = dist.FileStore(str(tmp_path / "store"), 1)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n = 2048
+        rng = np.random.default_rng(23)
+        f = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(np.complex64)
+        ft = torch.from_numpy(f).cuda()
+        try:
+            got = L2.lct2d_sharded(ft, ABCD5, (0.5, 1.5, -0.5, 0.5), transport="p2p").clone()
+        except (RuntimeError, NotImplementedError) as e:  # no symmetric-memory backend on this box
+            pytest.skip(f"symmetric memory unavailable: {e}")
+        ref = L2.lct2d(ft, ABCD5, (0.5, 1.5, -0.5, 0.5))
+        assert rel_l2(got.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
+    finally:
+        dist.destroy_process_group()
