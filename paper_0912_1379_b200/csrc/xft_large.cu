@@ -1090,7 +1090,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
 
 template <class C, int K, int LOGL, int W, int NBUF = 1, int MINB = 2>
 int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
-                  const double2* ptab, const double2* cptab, cudaStream_t st) {
+                  const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1) {
+  if (ld_out < 0) ld_out = ld;
   using Cfg = CluCfg<C, K, LOGL, W, NBUF, MINB>;
   constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
   if (R != (int64_t)K * Cfg::L || ncols % W || ncols / W > INT32_MAX || ld % 2) return XFT_ENOTSUP;
@@ -1138,7 +1139,7 @@ int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t l
   }
   const int ncl = groups < maxc ? groups : maxc;
   cfg.gridDim = dim3((unsigned)(K * ncl));
-  if (cudaLaunchKernelEx(&cfg, kern, map, static_cast<C*>(out), (long long)ld, groups, ck, ptab, cptab,
+  if (cudaLaunchKernelEx(&cfg, kern, map, static_cast<C*>(out), (long long)ld_out, groups, ck, ptab, cptab,
                          static_cast<const C*>(tb.tw)) != cudaSuccess)
     return XFT_ECUDA;
   return XFT_OK;
@@ -1147,18 +1148,18 @@ int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t l
 // tall columns through the cluster kernel: R = K * 1024 (K = 2..16), 64-byte row segments
 template <class C>
 int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
-                     const double2* ptab, const double2* cptab, cudaStream_t st) {
+                     const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1) {
   constexpr int W = sizeof(C) == 8 ? 8 : 4;
   if (!XFT_COLCLU || ncols % W) return XFT_ENOTSUP;
   switch (log2_of(R)) {
 #if XFT_CLU14 == 1
-    case 14: return launch_colclu<C, 8, 11, W / 2, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    case 14: return launch_colclu<C, 8, 11, W / 2, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
 #else
-    case 14: return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    case 14: return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
 #endif
-    case 13: return launch_colclu<C, 8, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
-    case 12: return launch_colclu<C, 4, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
-    case 11: return launch_colclu<C, 2, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st);
+    case 13: return launch_colclu<C, 8, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
+    case 12: return launch_colclu<C, 4, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
+    case 11: return launch_colclu<C, 2, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
     default: return XFT_ENOTSUP;
   }
 }
@@ -1214,6 +1215,22 @@ int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int6
 }  // namespace
 
 namespace xftb {
+
+// tall columns through the cluster kernel only, reading a [R][ncols] slab with
+// row stride ld and writing rows of stride ld_out (XFT_ENOTSUP if the cluster
+// path does not take this shape; nothing has been launched then)
+int run_lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, int64_t ld_out, int dtype,
+                         const double* abcd_host, int flags, cudaStream_t st) {
+  const int l = log2_of(R);
+  if ((int64_t(1) << l) != R || l <= LMAX || l > 14) return XFT_ENOTSUP;
+  const int bare = (flags & XFT_FLAG_BARE_FOURIER) ? 1 : 0;
+  const ColChirp k = col_chirp(abcd_host, R, bare);
+  const double2 *ptab = nullptr, *cptab = nullptr;
+  int rc = boundary_tables(R, &ptab, &cptab);
+  if (rc) return rc;
+  return dtype == XFT_C64 ? lct_cols_cluster<float2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out)
+                          : lct_cols_cluster<double2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out);
+}
 
 int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, int dtype,
                  const double* abcd_host, int flags, cudaStream_t st) {

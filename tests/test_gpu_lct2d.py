@@ -31,7 +31,9 @@ ABCD5 = (1.0, 0.25, 0.0, 1.0)
 
 @pytest.mark.parametrize("shape,dtype,tol", [((64, 64), np.complex128, 1e-12), ((2048, 256), np.complex128, 1e-12),
                                              ((256, 2048), np.complex64, 2e-5), ((4096, 64), np.complex64, 2e-5),
-                                             ((100, 48), np.complex128, 1e-12)])
+                                             ((100, 48), np.complex128, 1e-12),
+                                             # slab route (row pass into 8 column slabs, cluster columns)
+                                             ((2048, 2048), np.complex128, 1e-12), ((4096, 2048), np.complex64, 2e-5)])
 def test_lct2d_vs_oracle(torch, L2, shape, dtype, tol):
     rng = np.random.default_rng(5)
     f = (rng.normal(size=shape) + 1j * rng.normal(size=shape)).astype(dtype)
