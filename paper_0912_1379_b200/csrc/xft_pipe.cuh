@@ -1006,6 +1006,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     if constexpr (XFT_SKELETON == 2) {
       __syncthreads();
       first_barrier();
+      if constexpr (EARLY) stage_free();  // (the passes that would free the stage are skipped)
     } else {
       pipe_passes<Cfg, 0, EARLY>(v, xs, j, tw, first_barrier, stage_free);
     }
