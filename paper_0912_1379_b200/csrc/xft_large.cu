@@ -370,6 +370,103 @@ struct PostMehler {
   }
 };
 
+// Mehler four-step passes with walked Gaussian chirps: in the columns pass a
+// thread's samples a = j + s TR of column c sit at m = a M2 + c, so the kernel
+// lags (two monotone pieces) and the grid offsets m' = 2(k0 + m) - n + 1 are
+// linear in s and the values come from GaussWalk (xft_blue.cuh) instead of an
+// exp + table phasor per element.
+constexpr DD kInv2Pi{0.15915494309189535, -9.839338337591243e-18};
+
+struct OpColsMehlerH : OpCols<double2, GenMehlerH> {  // kernel spectrum, pass 1
+  static constexpr bool LOAD_LINE = true;
+  template <int E, int TR>
+  __device__ void load_line(long long tile, int w, int j, double2 (&v)[E]) const {
+    const int cb = M2 / W;
+    const long long b = tile / cb;
+    const int c = (int)(tile % cb) * W + w;
+    const OpMehlerRow p = gen.rows[gen.rowlist[b]];
+    const DD db = dd_mul(DD{-p.beta.y, 0.0}, kInv2Pi);
+    const double dl = (double)TR * M2;
+    const double2 S = gauss_val(p.beta.x, db, 2.0 * dl * dl);
+    GaussWalk wa;  // lags l = (j + s TR) M2 + c, s < E/2
+    const double la = (double)j * M2 + c;
+    wa.init(p.beta.x, db, la * la, dl * (2.0 * la + dl));
+#pragma unroll
+    for (int s = 0; s < E / 2; ++s) {
+      v[s] = la + s * dl < p.wn ? wa.W : make_double2(0.0, 0.0);
+      if (s < E / 2 - 1) wa.step(S);
+    }
+    GaussWalk wb;  // |l| = ((E - s) TR - j) M2 - c, s >= E/2 (ascending as s falls)
+    const double lb = (double)(TR - j) * M2 - c;
+    wb.init(p.beta.x, db, lb * lb, dl * (2.0 * lb + dl));
+#pragma unroll
+    for (int s = E - 1; s >= E / 2; --s) {
+      v[s] = lb + (E - 1 - s) * dl < p.wn ? wb.W : make_double2(0.0, 0.0);
+      if (s > E / 2) wb.step(S);
+    }
+  }
+};
+
+struct OpColsMehlerU : OpCols<double2, GenMehlerU> {  // windowed, weighted input, pass 1
+  static constexpr bool LOAD_LINE = true;
+  template <int E, int TR>
+  __device__ void load_line(long long tile, int w, int j, double2 (&v)[E]) const {
+    const int cb = M2 / W;
+    const long long b = tile / cb;
+    const int c = (int)(tile % cb) * W + w;
+    const long long row = gen.rowlist[b];
+    const OpMehlerRow p = gen.rows[row];
+    const long long n = gen.n;
+    const DD hh = dd_prod(gen.half, gen.half);
+    const double ag = p.gam.x * hh.hi;
+    const DD dg = dd_mul(dd_mul(hh, -p.gam.y), kInv2Pi);
+    const double dm = 2.0 * TR * M2;                              // m' step
+    const double mp0 = 2.0 * ((double)p.k0 + c + (double)j * M2) - (double)n + 1.0;
+    GaussWalk wg;
+    wg.init(ag, dg, mp0 * mp0, dm * (2.0 * mp0 + dm));
+    const double2 S = gauss_val(ag, dg, 2.0 * dm * dm);
+    const double2* src = gen.in + row * n;
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const long long m = (long long)(j + s * TR) * M2 + c;
+      double2 u = make_double2(0.0, 0.0);
+      if (m < p.wn) {
+        const long long k = p.k0 + m;
+        u = cmul_d(wg.W, src[p.sigma > 0 ? k : n - 1 - k]);
+      }
+      v[s] = u;
+      if (s < E - 1) wg.step(S);
+    }
+  }
+};
+
+struct OpColsInvMehler : OpColsInv<double2, PostMehler> {  // inverse columns + output weights
+  static constexpr bool STORE_LINE = true;
+  template <int E, int TR>
+  __device__ void store_line(long long tile, int w, int j, const double2 (&v)[E]) const {
+    const long long b = tile / (M2 / W);
+    const int c = (int)(tile % (M2 / W)) * W + w;
+    const long long row = post.rowlist[b];
+    const OpMehlerRow p = post.rows[row];
+    const long long n = post.n;
+    const DD hh = dd_prod(post.half, post.half);
+    const double ag = p.gam.x * hh.hi;
+    const DD dg = dd_mul(dd_mul(hh, -p.gam.y), kInv2Pi);
+    const double dm = 2.0 * TR * M2;
+    const double mp0 = 2.0 * ((double)p.k0 + c + (double)j * M2) - (double)n + 1.0;
+    GaussWalk wg;
+    wg.init(ag, dg, mp0 * mp0, dm * (2.0 * mp0 + dm));
+    wg.W = cmul_d(p.scale, wg.W);
+    const double2 S = gauss_val(ag, dg, 2.0 * dm * dm);
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const long long m = (long long)(j + s * TR) * M2 + c;
+      if (m < p.wn) post.out[row * n + p.k0 + m] = cmul_d(wg.W, v[s]);
+      if (s < E - 1) wg.step(S);
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
@@ -629,17 +726,17 @@ int run_large_mehler(const void* in, void* out, long long rows, const int* rowli
   const long long t1 = rows * (M2 / W), t2 = rows * (M1 / W);
   const double half = host_half_step(n);
   // kernel spectrum, permuted
-  OpCols<C, GenMehlerH> h1{GenMehlerH{prm, rowlist, sh.M}, hs.p, static_cast<const C*>(twm), M2, W, sh.M, 0};
+  OpColsMehlerH h1{{GenMehlerH{prm, rowlist, sh.M}, hs.p, static_cast<const C*>(twm), M2, W, sh.M, 0}};
   if ((rc = tile<C, true, true, -1>(sh.l1, t1, h1, st))) return rc;
   OpRowsPerm<C> h2{hs.p, M1, M2, W, sh.M};
   if ((rc = tile<C, false, false, -1>(sh.l2, t2, h2, st))) return rc;
   // data: columns, rows (forward x H inverse), inverse columns with the output weights
-  OpCols<C, GenMehlerU> u1{GenMehlerU{static_cast<const C*>(in), prm, rowlist, half, n}, us.p,
-                           static_cast<const C*>(twm), M2, W, sh.M, 0};
+  OpColsMehlerU u1{{GenMehlerU{static_cast<const C*>(in), prm, rowlist, half, n}, us.p,
+                    static_cast<const C*>(twm), M2, W, sh.M, 0}};
   if ((rc = tile<C, true, true, -1>(sh.l1, t1, u1, st))) return rc;
   OpRowsConv<C> u2{us.p, hs.p, sh.M, static_cast<const C*>(twm), M1, M2, W, sh.M};
   if ((rc = tile<C, false, false, -1>(sh.l2, t2, u2, st))) return rc;
-  OpColsInv<C, PostMehler> u3{us.p, PostMehler{static_cast<C*>(out), prm, rowlist, half, n}, M2, W, sh.M};
+  OpColsInvMehler u3{{us.p, PostMehler{static_cast<C*>(out), prm, rowlist, half, n}, M2, W, sh.M}};
   if ((rc = tile<C, true, true, +1>(sh.l1, t1, u3, st))) return rc;
   mehler_zero_kernel<<<(unsigned)rows, 256, 0, st>>>(static_cast<C*>(out), rowlist, prm, n);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;

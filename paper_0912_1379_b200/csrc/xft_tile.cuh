@@ -15,6 +15,8 @@
 //   C    Op::mid  (tile, line, a, C v)     optional: between a forward and an
 //                                          inverse FFT (Op::MID = true)
 #pragma once
+#include <type_traits>
+
 #include "xft_pipe.cuh"
 
 #ifndef XFT_TILE_PREFETCH
@@ -22,6 +24,19 @@
 #endif
 
 namespace xftb {
+
+// optional whole-line hooks of an operator: op.load_line<E, TR>(tile, w, j, v)
+// (Op::LOAD_LINE) / op.store_line<E, TR>(tile, w, j, v) (Op::STORE_LINE) see all
+// E samples j + s TR of a thread at once (generators that walk a quadratic
+// phase across s)
+template <class Op, class = void>
+struct HasLoadLine : std::false_type {};
+template <class Op>
+struct HasLoadLine<Op, std::void_t<decltype(Op::LOAD_LINE)>> : std::bool_constant<Op::LOAD_LINE> {};
+template <class Op, class = void>
+struct HasStoreLine : std::false_type {};
+template <class Op>
+struct HasStoreLine<Op, std::void_t<decltype(Op::STORE_LINE)>> : std::bool_constant<Op::STORE_LINE> {};
 
 template <class C, int LOGL, int E, int W, bool LOAD_COL, bool STORE_COL, int SIGN, class Op>
 __global__ void __launch_bounds__(W*((1 << LOGL) / E))
@@ -52,6 +67,8 @@ xft_tile_kernel(long long ntiles, Op op, const C* __restrict__ tw) {
       if (tile + gridDim.x < ntiles)
 #pragma unroll
         for (int s = 0; s < E; ++s) nxt[s] = op.load(tile + gridDim.x, w, j + s * TR);
+    } else if constexpr (HasLoadLine<Op>::value) {
+      op.template load_line<E, TR>(tile, w, j, v);
     } else {
 #pragma unroll
       for (int s = 0; s < E; ++s) v[s] = op.load(tile, w, j + s * TR);
@@ -62,7 +79,9 @@ xft_tile_kernel(long long ntiles, Op op, const C* __restrict__ tw) {
       for (int s = 0; s < E; ++s) v[s] = op.mid(tile, w, j + s * TR, v[s]);
       pipe_passes<Inv, 0>(v, smem + w * LS, j, tw, noop);
     }
-    if constexpr (LOAD_COL == STORE_COL) {
+    if constexpr (LOAD_COL == STORE_COL && HasStoreLine<Op>::value) {
+      op.template store_line<E, TR>(tile, w, j, v);
+    } else if constexpr (LOAD_COL == STORE_COL) {
 #pragma unroll
       for (int s = 0; s < E; ++s) op.store(tile, w, j + s * TR, v[s]);
     } else {
