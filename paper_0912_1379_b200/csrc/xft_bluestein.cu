@@ -2,6 +2,7 @@
 // LCT (xft/fftcore.py:84-100, 116-119) and the complex-z Mehler transform
 // (xft/dense.py:122-151).  Plan tables are built once per (device, n, sign,
 // dtype, mode) on the host in long double and cached (immutable).
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -252,6 +253,28 @@ struct MehlerPlan {
   int maxl = 0;
 };
 
+// grown on demand (outside capture: the bench and first calls size it), never shrunk
+void* stream_scratch(int dev, cudaStream_t st, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> pool;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = pool[{dev, st}];
+  if (e.second < bytes) {
+    if (e.first) {
+      if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
+      cudaFree(e.first);
+      e.first = nullptr;
+    }
+    if (cudaMalloc(&e.first, bytes) != cudaSuccess) {
+      e.first = nullptr;
+      e.second = 0;
+      return nullptr;
+    }
+    e.second = bytes;
+  }
+  return e.first;
+}
+
 int mehler_plan(int dev, int64_t batch, int64_t n, const double* z, int64_t z_stride, const MehlerPlan** out) {
   static std::mutex mu;
   static std::map<std::tuple<int, int64_t, int64_t, uint64_t>, MehlerPlan> cache;
@@ -331,10 +354,22 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const MehlerPlan* plan = nullptr;
   if ((rc = mehler_plan(dev, batch, n, z, z_stride, &plan))) return rc;
-  // per launched CTA one kernel-spectrum row of the largest in-CTA class
+  // per launched CTA one kernel-spectrum row of the largest in-CTA class, then
+  // the four-step classes' spectrum + data rows (2 x count x M)
   const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << plan->maxl) * sizeof(double2);
+  size_t large_bytes = 0;
+  for (const auto& cl : plan->classes)
+    if (cl.first > MAXL_C128) large_bytes = std::max(large_bytes, 2 * (size_t)cl.second * ((size_t)1 << cl.first) * 16);
   double2* d_hs = static_cast<double2*>(workspace);
-  if (!d_hs && cudaMallocAsync((void**)&d_hs, hs_bytes, st) != cudaSuccess) return XFT_ECUDA;
+  void* large_scratch = nullptr;
+  if (!d_hs) {
+    // persistent per-(device, stream) scratch: no allocation inside the call (or a
+    // captured CUDA graph); calls on one stream are ordered, so reuse is safe
+    char* base = static_cast<char*>(stream_scratch(dev, st, hs_bytes + large_bytes));
+    if (!base) return XFT_ECUDA;
+    d_hs = reinterpret_cast<double2*>(base);
+    large_scratch = base + hs_bytes;
+  }
   OpMehler op;
   op.rows = plan->rows;
   op.hscratch = d_hs;
@@ -344,11 +379,11 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
   for (const auto& cl : plan->classes) {
     const long long cnt = cl.second;
     rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan->list + off, op, st)
-                               : run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, st);
+                               : run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, st,
+                                                  large_scratch);
     if (rc) break;
     off += cnt;
   }
-  if (!workspace) cudaFreeAsync(d_hs, st);
   return rc;
 }
 

@@ -713,7 +713,7 @@ int large_chirpz(int lct, int bare, const C* in, C* out, int64_t batch, int64_t 
 
 // Mehler rows whose window needs M > in-CTA limit (complex128)
 int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm,
-                     int l, int64_t n, cudaStream_t st) {
+                     int l, int64_t n, cudaStream_t st, void* scratch) {
   using C = double2;
   constexpr int W = tile_w<C>();
   const Shape sh = split(l);
@@ -721,8 +721,18 @@ int run_large_mehler(const void* in, void* out, long long rows, const int* rowli
   const void* twm = nullptr;
   int rc = natural_twiddles(sh.M, XFT_C128, &twm);
   if (rc) return rc;
-  DevBuf<C> hs(st), us(st);
-  if ((rc = hs.alloc((size_t)rows * sh.M)) || (rc = us.alloc((size_t)rows * sh.M))) return rc;
+  DevBuf<C> hs(st), us(st);  // caller scratch (2 rows x M per row) when given, else stream-ordered
+  if (scratch) {
+    hs.p = static_cast<C*>(scratch);
+    us.p = hs.p + (size_t)rows * sh.M;
+    hs.st = us.st = nullptr;
+  } else if ((rc = hs.alloc((size_t)rows * sh.M)) || (rc = us.alloc((size_t)rows * sh.M))) {
+    return rc;
+  }
+  struct Release {  // caller scratch is not freed
+    DevBuf<C>& a; DevBuf<C>& b; bool own;
+    ~Release() { if (!own) { a.p = nullptr; b.p = nullptr; } }
+  } release{hs, us, scratch == nullptr};
   const long long t1 = rows * (M2 / W), t2 = rows * (M1 / W);
   const double half = host_half_step(n);
   // kernel spectrum, permuted
