@@ -377,7 +377,11 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = total_ms / args.steps
     samples = samples_of(work)
     value = world * samples / (ms_per_step * 1e-3) / 1e6
-    launches_per_step = sum({"lct": 2, "mehler": 2, "lct2d": 4}[it.kind] for it in work)
+    # our kernels per step (ncu launch lists, profiles/r1/final/launches_*.txt): a row batch is one
+    # xft_pipe_kernel; config 3's Mehler step is 2 xft_blue_kernel + 10 xft_tile_kernel + 2 zero-fill
+    # kernels; the single-GPU 2-D step is 1 row kernel + 8 cluster column kernels (one per slab),
+    # the sharded one 1 row kernel + 1 column kernel per rank
+    launches_per_step = sum({"lct": 1, "mehler": 14, "lct2d": 9 if world == 1 else 2}[it.kind] for it in work)
 
     # end-to-end through the public host-buffer API: pinned host in, result back on the host
     e2e_steps = max(2, min(args.steps, args.e2e_steps))
