@@ -215,3 +215,21 @@ def test_large_pow2_lct(torch, X, n, dtype):
     got = X.ops.lct_rows(dev(torch, f), abcd).cpu().numpy()
     _, ref = O.fast_lct_rows(abcd, f.astype(complex))
     assert max_row_rel_l2(got, ref) <= tol
+
+
+def test_mehler_config3_truth(torch, X):
+    """Config-3 rows with unit-modulus Mehler kernels (z ~ -0.5i .. -0.65i), where the float64
+    dense formula itself loses up to ~6e-13, against a long-double evaluation of the same formula
+    (tests/golden/make_mehler_truth.py): the GPU result must be within 1e-12 of the truth."""
+    import os
+
+    from paper_0912_1379_b200 import workloads
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "mehler_truth_cfg3.npz"))
+    c3 = workloads.config3()
+    rows = [int(r) for r in g["rows"]]
+    js = g["js"]
+    got = X.mehler_rows(dev(torch, c3.values[rows]), c3.extra["z"][rows]).cpu().numpy()
+    for i, r in enumerate(rows):
+        truth = g[f"truth_{r}"]
+        assert rel_l2(got[i, js], truth) <= 1e-12, (r, rel_l2(got[i, js], truth))
