@@ -48,6 +48,9 @@
 #ifndef XFT_MIRROR
 #define XFT_MIRROR 1  // mirror lane map + shared rounding corrections (see PipeCfg::MIRROR)
 #endif
+#ifndef XFT_C128_EARLY
+#define XFT_C128_EARLY 0  // c128 single-stage CTAs: issue the next tile's load after the last exchange read
+#endif
 #ifndef XFT_SPLIT
 #define XFT_SPLIT 1  // split next-row prefetch for single-row CTAs (see PipeCfg::SPLIT)
 #endif
@@ -996,7 +999,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     // single stage: the next tile's load starts once the last exchange has been
     // read (c64; for c128 the barrier in front of the fp64-heavy last pass
     // costs more than the earlier load gains, measured 137 -> 146 us at cfg2)
-    constexpr bool EARLY = S == 1 && !Cfg::C128;
+    constexpr bool EARLY = S == 1 && (!Cfg::C128 || XFT_C128_EARLY);
     auto stage_free = [&]() {
       if (tid == 0 && tile + G < ntiles) {
         if constexpr (SPLIT > 0) issue_b(tile + G);
