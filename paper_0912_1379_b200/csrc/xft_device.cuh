@@ -294,27 +294,53 @@ template <int SIGN, class C> __device__ __forceinline__ void dft16_44(C* v) {
   for (int i = 0; i < 16; ++i) v[i] = r[i];
 }
 
+// the second half of dft16_44: internal twiddles and the 4-point DFTs along k1
+// (for callers that ran the column stage themselves)
+template <int SIGN, class C> __device__ __forceinline__ void dft16_44_rows(C* v) {
+  v[4 + 1] = w16odd<SIGN, 1>(v[4 + 1]);
+  v[4 + 2] = w8<SIGN, 1>(v[4 + 2]);
+  v[4 + 3] = w16odd<SIGN, 3>(v[4 + 3]);
+  v[8 + 1] = w8<SIGN, 1>(v[8 + 1]);
+  v[8 + 2] = w8<SIGN, 2>(v[8 + 2]);
+  v[8 + 3] = w8<SIGN, 3>(v[8 + 3]);
+  v[12 + 1] = w16odd<SIGN, 3>(v[12 + 1]);
+  v[12 + 2] = w8<SIGN, 3>(v[12 + 2]);
+  {
+    const C t = w16odd<SIGN, 1>(v[12 + 3]);
+    v[12 + 3] = mk(-t.x, -t.y);
+  }
+  C r[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    C a = v[4 * k1], b = v[4 * k1 + 1], c = v[4 * k1 + 2], d = v[4 * k1 + 3];
+    dft4<SIGN>(a, b, c, d);
+    r[k1] = a; r[k1 + 4] = b; r[k1 + 8] = c; r[k1 + 12] = d;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = r[i];
+}
+
 template <int SIGN, class C> __device__ __forceinline__ void dft16(C* v) {
   if constexpr (XFT_DFT16_44) {
     dft16_44<SIGN>(v);
-    return;
-  }
-  C e[8], o[8];
+  } else {
+    C e[8], o[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
-  dft8<SIGN>(e);
-  dft8<SIGN>(o);
-  o[1] = w16odd<SIGN, 1>(o[1]);
-  o[2] = w8<SIGN, 1>(o[2]);
-  o[3] = w16odd<SIGN, 3>(o[3]);
-  o[4] = w8<SIGN, 2>(o[4]);
-  o[5] = w16odd<SIGN, 5>(o[5]);
-  o[6] = w8<SIGN, 3>(o[6]);
-  o[7] = w16odd<SIGN, 7>(o[7]);
+    for (int i = 0; i < 8; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
+    dft8<SIGN>(e);
+    dft8<SIGN>(o);
+    o[1] = w16odd<SIGN, 1>(o[1]);
+    o[2] = w8<SIGN, 1>(o[2]);
+    o[3] = w16odd<SIGN, 3>(o[3]);
+    o[4] = w8<SIGN, 2>(o[4]);
+    o[5] = w16odd<SIGN, 5>(o[5]);
+    o[6] = w8<SIGN, 3>(o[6]);
+    o[7] = w16odd<SIGN, 7>(o[7]);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    v[i] = cadd(e[i], o[i]);
-    v[i + 8] = csub(e[i], o[i]);
+    for (int i = 0; i < 8; ++i) {
+      v[i] = cadd(e[i], o[i]);
+      v[i + 8] = csub(e[i], o[i]);
+    }
   }
 }
 

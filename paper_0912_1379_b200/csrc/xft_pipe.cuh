@@ -413,6 +413,12 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 // FREE_EARLY: after the last exchange's reads, one more barrier and free_hook()
 // -- the buffer is dead from there on, so a single-stage caller can start the
 // next tile's load under the last pass and the epilogue.
+#ifndef XFT_NOTW
+#define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
+#endif
+#ifndef XFT_FUSE_TW
+#define XFT_FUSE_TW 1  // c128: inter-pass twiddles fused into the first butterfly stage (FMA chains)
+#endif
 #ifndef XFT_TWGEN
 #define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
 #endif
@@ -429,6 +435,9 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
   constexpr int NS = Cfg::ns(P);
   constexpr int NB = E / R;
   constexpr bool LAST = (P == Cfg::NPASS - 1);
+  // c128 LCT-mode radix-16 passes: twiddles fused into the butterfly's first stage
+  constexpr bool FUSED = XFT_FUSE_TW && Cfg::C128 && R == 16 && XFT_DFT16_44 && NS > 1 && XFT_SKELETON == 0 &&
+                         !XFT_NOTW && XFT_TWGEN && Cfg::MODE != MODE_DFT;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int i = j + b * TR;
@@ -436,9 +445,6 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     C u[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) u[t] = v[b + t * NB];
-#ifndef XFT_NOTW
-#define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
-#endif
     if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW && XFT_TWGEN && (!Cfg::C128 || Cfg::MODE != MODE_DFT) && R >= 8) {
       // w^t from w and w^{8b} (table): w^2..w^7 by a product tree of depth 3,
       // w^{8b+r} = w^{8b} w^r.  R/8 loads instead of R - 1 (fewer registers held
@@ -459,14 +465,36 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
       lo[5] = cmul(lo[4], lo[1]);
       lo[6] = cmul(lo[4], lo[2]);
       lo[7] = cmul(lo[4], lo[3]);
+      if constexpr (FUSED) {
+        // twiddles folded into the first 4-point stage of the 4 x 4 butterfly:
+        // x0 + w2 u2 = fma chain (no separate product), x0 - w2 u2 = 2 x0 - (x0 + w2 u2)
+        const C h = ld(8);
 #pragma unroll
-      for (int t = 1; t < 8; ++t) u[t] = cmul(u[t], lo[t]);
+        for (int n2 = 0; n2 < 4; ++n2) {
+          const C x0 = n2 == 0 ? u[0] : cmul(u[n2], lo[n2]);
+          const C x1 = cmul(u[4 + n2], lo[4 + n2]);
+          const C w2 = n2 == 0 ? h : cmul(h, lo[n2]);
+          const C w3 = cmul(h, lo[4 + n2]);
+          const C a = u[8 + n2], b = u[12 + n2];
+          const C t0 = mk(fma(a.x, w2.x, fma(-a.y, w2.y, x0.x)), fma(a.x, w2.y, fma(a.y, w2.x, x0.y)));
+          const C t1 = mk(fma(2.0, x0.x, -t0.x), fma(2.0, x0.y, -t0.y));
+          const C t2 = mk(fma(b.x, w3.x, fma(-b.y, w3.y, x1.x)), fma(b.x, w3.y, fma(b.y, w3.x, x1.y)));
+          const C t3 = rot<Cfg::SIGN>(mk(fma(2.0, x1.x, -t2.x), fma(2.0, x1.y, -t2.y)));
+          u[n2] = cadd(t0, t2);
+          u[8 + n2] = csub(t0, t2);
+          u[4 + n2] = cadd(t1, t3);
+          u[12 + n2] = csub(t1, t3);
+        }
+      } else {
 #pragma unroll
-      for (int b = 1; b < R / 8; ++b) {
-        const C h = ld(8 * b);
-        u[8 * b] = cmul(u[8 * b], h);
+        for (int t = 1; t < 8; ++t) u[t] = cmul(u[t], lo[t]);
 #pragma unroll
-        for (int r = 1; r < 8; ++r) u[8 * b + r] = cmul(u[8 * b + r], cmul(h, lo[r]));
+        for (int b = 1; b < R / 8; ++b) {
+          const C h = ld(8 * b);
+          u[8 * b] = cmul(u[8 * b], h);
+#pragma unroll
+          for (int r = 1; r < 8; ++r) u[8 * b + r] = cmul(u[8 * b + r], cmul(h, lo[r]));
+        }
       }
     } else if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW) {
       const C* twp = tw + Cfg::twoff(P) + k;
@@ -479,7 +507,8 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
         u[t] = cmul(u[t], w);
       }
     }
-    if constexpr (XFT_SKELETON == 0) dft_r<R, Cfg::SIGN>(u);
+    if constexpr (FUSED) dft16_44_rows<Cfg::SIGN>(u);  // first stage done above
+    else if constexpr (XFT_SKELETON == 0) dft_r<R, Cfg::SIGN>(u);
 #pragma unroll
     for (int t = 0; t < R; ++t) v[b + t * NB] = u[t];
   }
