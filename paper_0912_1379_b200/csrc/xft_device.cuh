@@ -164,6 +164,20 @@ template <> struct phase_of<double2> {
   static __device__ __forceinline__ double2 eval(double phi) { return unit_phase(phi); }
 };
 
+// x + a w (complex) as FMA chains, and 2 x - t
+__device__ __forceinline__ double2 cfma(double2 a, double2 w, double2 x) {
+  return make_double2(fma(a.x, w.x, fma(-a.y, w.y, x.x)), fma(a.x, w.y, fma(a.y, w.x, x.y)));
+}
+__device__ __forceinline__ float2 cfma(float2 a, float2 w, float2 x) {  // FFMA2 x 2
+  return p_fma(make_float2(-a.y, a.x), make_float2(w.y, w.y), p_fma(a, make_float2(w.x, w.x), x));
+}
+__device__ __forceinline__ double2 ctwice_minus(double2 x, double2 t) {
+  return make_double2(fma(2.0, x.x, -t.x), fma(2.0, x.y, -t.y));
+}
+__device__ __forceinline__ float2 ctwice_minus(float2 x, float2 t) {
+  return p_fma(x, make_float2(2.0f, 2.0f), make_float2(-t.x, -t.y));
+}
+
 // ---------------------------------------------------------------------------
 // in-register DFT butterflies, X_t = sum_s x_s e^{SIGN 2 pi i s t / R}
 // ---------------------------------------------------------------------------

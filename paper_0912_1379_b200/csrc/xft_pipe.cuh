@@ -419,6 +419,9 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 #ifndef XFT_FUSE_TW
 #define XFT_FUSE_TW 1  // c128: inter-pass twiddles fused into the first butterfly stage (FMA chains)
 #endif
+#ifndef XFT_FUSE_TW64
+#define XFT_FUSE_TW64 1  // the same for c64 (packed FP32x2 FMA chains)
+#endif
 #ifndef XFT_TWGEN
 #define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
 #endif
@@ -436,8 +439,8 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
   constexpr int NB = E / R;
   constexpr bool LAST = (P == Cfg::NPASS - 1);
   // c128 LCT-mode radix-16 passes: twiddles fused into the butterfly's first stage
-  constexpr bool FUSED = XFT_FUSE_TW && Cfg::C128 && R == 16 && XFT_DFT16_44 && NS > 1 && XFT_SKELETON == 0 &&
-                         !XFT_NOTW && XFT_TWGEN && Cfg::MODE != MODE_DFT;
+  constexpr bool FUSED = (Cfg::C128 ? XFT_FUSE_TW : XFT_FUSE_TW64) && R == 16 && XFT_DFT16_44 && NS > 1 &&
+                         XFT_SKELETON == 0 && !XFT_NOTW && XFT_TWGEN && (!Cfg::C128 || Cfg::MODE != MODE_DFT);
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int i = j + b * TR;
@@ -476,10 +479,10 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
           const C w2 = n2 == 0 ? h : cmul(h, lo[n2]);
           const C w3 = cmul(h, lo[4 + n2]);
           const C a = u[8 + n2], b = u[12 + n2];
-          const C t0 = mk(fma(a.x, w2.x, fma(-a.y, w2.y, x0.x)), fma(a.x, w2.y, fma(a.y, w2.x, x0.y)));
-          const C t1 = mk(fma(2.0, x0.x, -t0.x), fma(2.0, x0.y, -t0.y));
-          const C t2 = mk(fma(b.x, w3.x, fma(-b.y, w3.y, x1.x)), fma(b.x, w3.y, fma(b.y, w3.x, x1.y)));
-          const C t3 = rot<Cfg::SIGN>(mk(fma(2.0, x1.x, -t2.x), fma(2.0, x1.y, -t2.y)));
+          const C t0 = cfma(a, w2, x0);
+          const C t1 = ctwice_minus(x0, t0);
+          const C t2 = cfma(b, w3, x1);
+          const C t3 = rot<Cfg::SIGN>(ctwice_minus(x1, t2));
           u[n2] = cadd(t0, t2);
           u[8 + n2] = csub(t0, t2);
           u[4 + n2] = cadd(t1, t3);
