@@ -422,6 +422,12 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 #ifndef XFT_FUSE_TW64
 #define XFT_FUSE_TW64 1  // the same for c64 (packed FP32x2 FMA chains)
 #endif
+#ifndef XFT_TWLOAD1
+#define XFT_TWLOAD1 1  // c128: w^8 = (w^4)^2 too, one table load per butterfly (A/B: -0.5% n=4096, -1.5% n=8192)
+#endif
+#ifndef XFT_TWLOAD4
+#define XFT_TWLOAD4 0  // 1: w^2 and w^4 loaded too (two loads for two multiplies)
+#endif
 #ifndef XFT_TWGEN
 #define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
 #endif
@@ -462,16 +468,16 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
       };
       C lo[8];
       lo[1] = ld(1);
-      lo[2] = cmul(lo[1], lo[1]);
+      lo[2] = XFT_TWLOAD4 ? ld(2) : cmul(lo[1], lo[1]);
       lo[3] = cmul(lo[2], lo[1]);
-      lo[4] = cmul(lo[2], lo[2]);
+      lo[4] = XFT_TWLOAD4 ? ld(4) : cmul(lo[2], lo[2]);
       lo[5] = cmul(lo[4], lo[1]);
       lo[6] = cmul(lo[4], lo[2]);
       lo[7] = cmul(lo[4], lo[3]);
       if constexpr (FUSED) {
         // twiddles folded into the first 4-point stage of the 4 x 4 butterfly:
         // x0 + w2 u2 = fma chain (no separate product), x0 - w2 u2 = 2 x0 - (x0 + w2 u2)
-        const C h = ld(8);
+        const C h = (Cfg::C128 ? XFT_TWLOAD1 : 0) ? cmul(lo[4], lo[4]) : ld(8);  // c128: one table load
 #pragma unroll
         for (int n2 = 0; n2 < 4; ++n2) {
           const C x0 = n2 == 0 ? u[0] : cmul(u[n2], lo[n2]);
