@@ -45,6 +45,27 @@
 #endif
 #include "xft_tma.cuh"
 
+#ifndef XFT_NOTW
+#define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
+#endif
+#ifndef XFT_FUSE_TW
+#define XFT_FUSE_TW 1  // c128: inter-pass twiddles fused into the first butterfly stage (FMA chains)
+#endif
+#ifndef XFT_FUSE_TW64
+#define XFT_FUSE_TW64 1  // the same for c64 (packed FP32x2 FMA chains)
+#endif
+#ifndef XFT_TWBASE
+#define XFT_TWBASE 1  // c128 row kernels: per-thread base twiddles held across rows (see pipe_pass)
+#endif
+#ifndef XFT_TWLOAD1
+#define XFT_TWLOAD1 1  // c128: w^8 = (w^4)^2 too, one table load per butterfly (A/B: -0.5% n=4096, -1.5% n=8192)
+#endif
+#ifndef XFT_TWLOAD4
+#define XFT_TWLOAD4 0  // 1: w^2 and w^4 loaded too (two loads for two multiplies)
+#endif
+#ifndef XFT_TWGEN
+#define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
+#endif
 #ifndef XFT_MIRROR
 #define XFT_MIRROR 1  // mirror lane map + shared rounding corrections (see PipeCfg::MIRROR)
 #endif
@@ -395,6 +416,9 @@ struct PipeCfg {
   // -x_k exactly), hence the chirp-argument rounding corrections: each lane
   // computes 8 of its 16 and takes the other 8 from its partner by shuffle.
   static constexpr bool MIRROR = SPLITOK_ && C128 && MODE == MODE_LCT && TR % 32 == 0 && XFT_MIRROR;
+  // (single-row CTAs only: at two CTAs/SM, n = 4096, the held registers spill and cost 6%; n = 8192 gains 4%)
+  static constexpr bool TWBASE = SPLITOK_ && C128 && MODE == MODE_LCT && XFT_TWBASE && XFT_TWGEN && E == 16 &&
+                                 NPASS <= E && MINB_ == 1;
   static constexpr size_t SMEM = MAIN + size_t(SPLIT) * sizeof(C);
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
@@ -413,24 +437,6 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 // FREE_EARLY: after the last exchange's reads, one more barrier and free_hook()
 // -- the buffer is dead from there on, so a single-stage caller can start the
 // next tile's load under the last pass and the epilogue.
-#ifndef XFT_NOTW
-#define XFT_NOTW 0  // tuning only: 1 = skip the inter-pass twiddles
-#endif
-#ifndef XFT_FUSE_TW
-#define XFT_FUSE_TW 1  // c128: inter-pass twiddles fused into the first butterfly stage (FMA chains)
-#endif
-#ifndef XFT_FUSE_TW64
-#define XFT_FUSE_TW64 1  // the same for c64 (packed FP32x2 FMA chains)
-#endif
-#ifndef XFT_TWLOAD1
-#define XFT_TWLOAD1 1  // c128: w^8 = (w^4)^2 too, one table load per butterfly (A/B: -0.5% n=4096, -1.5% n=8192)
-#endif
-#ifndef XFT_TWLOAD4
-#define XFT_TWLOAD4 0  // 1: w^2 and w^4 loaded too (two loads for two multiplies)
-#endif
-#ifndef XFT_TWGEN
-#define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
-#endif
 #ifndef XFT_TWPRE
 #define XFT_TWPRE 0  // 1: load the next pass's twiddles between the exchange stores and the barrier
 #endif
@@ -467,7 +473,10 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
         return Cfg::SIGN > 0 ? cconj(w) : w;
       };
       C lo[8];
-      lo[1] = ld(1);
+      // row kernels (c128): w^1 of every twiddled pass is a per-thread constant,
+      // loaded once per kernel into wpre[P] by the caller (no load per row)
+      if constexpr (Cfg::TWBASE) lo[1] = wpre[P];
+      else lo[1] = ld(1);
       lo[2] = XFT_TWLOAD4 ? ld(2) : cmul(lo[1], lo[1]);
       lo[3] = cmul(lo[2], lo[1]);
       lo[4] = XFT_TWLOAD4 ? ld(4) : cmul(lo[2], lo[2]);
@@ -988,6 +997,15 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     }
   }
 
+  C wbase[Cfg::E];  // TWBASE: wbase[P] = w^1 of pass P for this thread (constant over rows)
+  if constexpr (Cfg::TWBASE) {
+#pragma unroll
+    for (int p = 1; p < Cfg::NPASS; ++p) {
+      const int nsp = Cfg::ns(p);
+      C w = __ldg(tw + Cfg::twoff(p) + (j & (nsp - 1)));
+      wbase[p] = Cfg::SIGN > 0 ? cconj(w) : w;
+    }
+  }
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int st = it % S;
     if constexpr (Cfg::MODE == MODE_LCT) {
@@ -1049,7 +1067,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
       first_barrier();
       if constexpr (EARLY) stage_free();  // (the passes that would free the stage are skipped)
     } else {
-      pipe_passes<Cfg, 0, EARLY>(v, xs, j, tw, first_barrier, stage_free);
+      pipe_passes_w<Cfg, 0, EARLY>(v, xs, j, tw, first_barrier, stage_free, wbase);
     }
     if constexpr (S == 1 && !EARLY) {
       __syncthreads();
