@@ -251,9 +251,9 @@ __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abc
   c.gf = (v - vi) * kC128[0];
   c.gturn = v * (1.0 / C128_TABN);
   c.gabs = g_abs(b, k);
-  double s, co;
-  sincospi(v * (2.0 / C128_TABN), &s, &co);
-  c.g = make_double2(c.gabs * co, c.gabs * s);
+  // G = |G| e^{2 pi i v / T}: the table path (v / T is exact, |v / T| < 1/2), no libm sincospi
+  const double2 eg = turn_phasor(v * (1.0 / C128_TABN), 0.0, 0.0, tab);
+  c.g = make_double2(c.gabs * eg.x, c.gabs * eg.y);
   // smooth chirp rates (turns per m^2) and the walk's second-difference phasors
   const DD h2i = dd_mul(dd_prod(k.half, k.half), DD{0.15915494309189535, -9.839338337591243e-18});
   const DD din = dd_mul(h2i, c.cin);
