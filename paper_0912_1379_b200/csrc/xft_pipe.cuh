@@ -378,6 +378,30 @@ struct TurnWalk {
   }
 };
 
+// The same walk with the differences rounded to 32 bits (one add each per
+// element): the phase drifts by at most s^2/2 units of 2^-32 turn over s
+// steps (<= 1.2e-7 turn at s = 31), far inside the c64 budget.
+struct TurnWalk32 {
+  uint32_t t, d, dd;
+  __device__ __forceinline__ TurnWalk32(unsigned long long dq, int off0, int S2, unsigned long long lin0,
+                                        unsigned long long lstep) {
+    const TurnWalk w(dq, off0, S2, lin0, lstep);
+    t = w.t;
+    d = (uint32_t)((w.d + (1ull << 31)) >> 32);
+    dd = (uint32_t)((w.dd + (1ull << 31)) >> 32);
+  }
+  __device__ __forceinline__ uint32_t next() {
+    const uint32_t r = t;
+    t += d;
+    d += dd;
+    return r;
+  }
+};
+#ifndef XFT_WALK32
+#define XFT_WALK32 1
+#endif
+using ChirpTurnWalk = std::conditional_t<XFT_WALK32 != 0, TurnWalk32, TurnWalk>;
+
 // ---------------------------------------------------------------------------
 // configuration
 // ---------------------------------------------------------------------------
@@ -710,7 +734,7 @@ __device__ __forceinline__ void pre_apply(typename Cfg::C (&v)[Cfg::E], Load&& l
     if constexpr (Cfg::MODE == MODE_LCT) {
       if constexpr (!Cfg::C128) {
         // boundary phase (-1)^k e^{-i pi k/n} rides on the walk's linear term
-        TurnWalk w(rcs.dq_in, tc.off0, 2 * TR, (unsigned long long)tc.bt0 << 32, 1ull << (63 - Cfg::LE));
+        ChirpTurnWalk w(rcs.dq_in, tc.off0, 2 * TR, (unsigned long long)tc.bt0 << 32, 1ull << (63 - Cfg::LE));
 #pragma unroll
         for (int s = 0; s < E; ++s) v[s] = cmul(walk_phasor(w.next()), ld(s));
       } else {
@@ -826,7 +850,7 @@ __device__ __forceinline__ void post_apply(typename Cfg::C (&v)[Cfg::E], int j, 
       return;
     }
     if constexpr (!Cfg::C128) {
-      TurnWalk w(rcs.dq_out, tc.off0, 2 * TR, (unsigned long long)(tc.bt0 + rcs.gq) << 32, 1ull << (63 - Cfg::LE));
+      ChirpTurnWalk w(rcs.dq_out, tc.off0, 2 * TR, (unsigned long long)(tc.bt0 + rcs.gq) << 32, 1ull << (63 - Cfg::LE));
       const float2 g = make_float2(rcs.gabs, rcs.gabs);
 #pragma unroll
       for (int s = 0; s < E; ++s) emit(s, cmul(walk_phasor(w.next()), p_mul(v[s], g)));
