@@ -66,7 +66,14 @@ __device__ __forceinline__ void tma_prefetch_l2(const void* src_gmem, uint32_t b
 }
 
 // streaming store (evict-first): outputs are not re-read by this kernel
-__device__ __forceinline__ void st_stream(float2* p, float2 v) { __stcs(p, v); }
-__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+#ifndef XFT_STCS
+#define XFT_STCS 1  // 0: plain write-back stores for the row outputs (tuning)
+#endif
+__device__ __forceinline__ void st_stream(float2* p, float2 v) {
+  if (XFT_STCS) __stcs(p, v); else *p = v;
+}
+__device__ __forceinline__ void st_stream(double2* p, double2 v) {
+  if (XFT_STCS) __stcs(p, v); else *p = v;
+}
 
 }  // namespace xftb
