@@ -23,7 +23,6 @@ import math
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -61,47 +60,61 @@ _REASONS = {
 }
 
 
-class ClockSampler:
-    def __init__(self, index: int, period_s: float = 0.01):
-        self.samples = []
-        self.reasons = 0
-        self.max_mhz = None
-        self._stop = threading.Event()
-        self._thr = None
-        try:
-            import pynvml
+def _clock_worker(index, period, stop, out):
+    """Child process: samples NVML SM clocks and throttle reasons until `stop` is set
+    (a separate process, so the GIL held by blocking graph launches cannot starve it)."""
+    try:
+        import pynvml
 
-            pynvml.nvmlInit()
-            self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self._nv = None
-        self.period = period_s
-
-    def _run(self):
-        nv = self._nv
-        while not self._stop.is_set():
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        samples = []
+        while not stop.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                samples.append((time.perf_counter(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
             except Exception:
                 pass
-            time.sleep(self.period)
+            time.sleep(period)
+        out.put((samples, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
+    except Exception:
+        out.put(None)
+
+
+class ClockSampler:
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons, self.max_mhz, self.ok = [], 0, None, False
 
     def __enter__(self):
-        if self._nv is not None:
-            self._thr = threading.Thread(target=self._run, daemon=True)
-            self._thr.start()
+        import multiprocessing as mp
+
+        ctx = mp.get_context("fork")
+        self._stop, self._q = ctx.Event(), ctx.Queue()
+        self._p = ctx.Process(target=_clock_worker, args=(self.index, self.period, self._stop, self._q), daemon=True)
+        self._p.start()
+        time.sleep(0.05)  # the child is sampling before the timed region starts
+        self._t0 = time.perf_counter()
         return self
 
     def __exit__(self, *a):
+        t1 = time.perf_counter()
         self._stop.set()
-        if self._thr is not None:
-            self._thr.join()
+        try:
+            res = self._q.get(timeout=10)
+        except Exception:
+            res = None
+        self._p.join(timeout=10)
+        if res is not None:
+            rows, self.max_mhz = res
+            inside = [r for r in rows if self._t0 <= r[0] <= t1]  # the timed region only
+            self.samples = [r[1] for r in inside]
+            for r in inside:
+                self.reasons |= r[2]
+            self.ok = True
 
     def summary(self):
-        if self._nv is None:
+        if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
         names = [v for k, v in _REASONS.items() if self.reasons & k and v != "gpu_idle"]
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
@@ -319,6 +332,7 @@ def run_ours(args, rank, world, local_rank):
             return run
         graphs = {}
         per_set = [[(work[k], sets[i][k]) for k in idx] for i in range(nsets)]
+        lanes = [torch.cuda.Stream(dev) for _ in idx]
 
         def graph(reps):
             if reps not in graphs:
@@ -329,9 +343,22 @@ def run_ours(args, rank, world, local_rank):
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
-                    for r in range(reps):
-                        for it, st in per_set[r % nsets]:
-                            launch(it, st)
+                    if len(idx) > 1 and args.overlap:
+                        # the step's batches are independent: each item's launches are chained
+                        # on its own stream (fork/join around the whole graph), so one batch's
+                        # kernel can start on the SMs another's tail leaves idle
+                        for lane in lanes:
+                            lane.wait_stream(stream)
+                        for r in range(reps):
+                            for lane, (it, st) in zip(lanes, per_set[r % nsets]):
+                                with torch.cuda.stream(lane):
+                                    launch(it, st)
+                        for lane in lanes:
+                            stream.wait_stream(lane)
+                    else:
+                        for r in range(reps):
+                            for it, st in per_set[r % nsets]:
+                                launch(it, st)
                 graphs[reps] = g
             return graphs[reps]
 
@@ -467,7 +494,9 @@ def run_ours(args, rank, world, local_rank):
                                     else f"row-sharded x{world}, " + ("row-kernel NVLink peer stores (symmetric memory)"
                                                                      if args.transport == "p2p" and world > 1
                                                                      else "one NCCL all_to_all_single")),
-                       timing="CUDA graphs" if capturable else "direct launches"),
+                       timing=("CUDA graphs" if capturable else "direct launches")
+                       + (", step items on independent streams" if capturable and args.overlap and len(work) > 1
+                          else "")),
         "roofline": roof, "per_dtype": per, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "Msamples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "api": "ops.lct_host -> xft_lct_host" if work[0].kind == "lct"
@@ -489,6 +518,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=None, help="CPU baseline rows per item (default: full batch)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="1: the step's independent batches (c64, c128) on their own streams inside the graph")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="cfg5 under torchrun: row-kernel NVLink peer stores (p2p) or NCCL all_to_all")
     args = ap.parse_args()
