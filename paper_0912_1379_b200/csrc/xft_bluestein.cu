@@ -253,6 +253,38 @@ struct MehlerPlan {
   int maxl = 0;
 };
 
+// internal streams of a Mehler call on caller stream `st` (fork/join events),
+// created once per (device, caller stream) and grown to the class count
+struct SideStreams {
+  std::mutex mu;
+  std::vector<cudaStream_t> st;
+  std::vector<cudaEvent_t> join;
+  cudaEvent_t fork = nullptr;
+  bool ok = true;
+};
+SideStreams& side_streams(int dev, cudaStream_t caller, int count) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SideStreams*> pool;
+  std::lock_guard<std::mutex> lock(mu);
+  SideStreams*& p = pool[{dev, caller}];
+  if (!p) {
+    p = new SideStreams();
+    if (cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming) != cudaSuccess) p->ok = false;
+  }
+  while (p->ok && (int)p->st.size() < count) {
+    cudaStream_t s = nullptr;
+    cudaEvent_t e = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      p->ok = false;
+      break;
+    }
+    p->st.push_back(s);
+    p->join.push_back(e);
+  }
+  return *p;
+}
+
 // grown on demand (outside capture: the bench and first calls size it), never shrunk
 void* stream_scratch(int dev, cudaStream_t st, size_t bytes) {
   static std::mutex mu;
@@ -357,33 +389,60 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
   // per launched CTA one kernel-spectrum row of the largest in-CTA class, then
   // the four-step classes' spectrum + data rows (2 x count x M)
   const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << plan->maxl) * sizeof(double2);
-  size_t large_bytes = 0;
-  for (const auto& cl : plan->classes)
-    if (cl.first > MAXL_C128) large_bytes = std::max(large_bytes, 2 * (size_t)cl.second * ((size_t)1 << cl.first) * 16);
-  double2* d_hs = static_cast<double2*>(workspace);
-  void* large_scratch = nullptr;
-  if (!d_hs) {
-    // persistent per-(device, stream) scratch: no allocation inside the call (or a
-    // captured CUDA graph); calls on one stream are ordered, so reuse is safe
-    char* base = static_cast<char*>(stream_scratch(dev, st, hs_bytes + large_bytes));
-    if (!base) return XFT_ECUDA;
-    d_hs = reinterpret_cast<double2*>(base);
-    large_scratch = base + hs_bytes;
+  size_t large_bytes = 0, all_bytes = 0;
+  for (const auto& cl : plan->classes) {
+    const size_t b = cl.first <= MAXL_C128 ? hs_bytes : 2 * (size_t)cl.second * ((size_t)1 << cl.first) * 16;
+    if (cl.first > MAXL_C128) large_bytes = std::max(large_bytes, b);
+    all_bytes += b;
   }
   OpMehler op;
   op.rows = plan->rows;
-  op.hscratch = d_hs;
   op.half = host_half_step(n);
   op.n = (int)n;
-  size_t off = 0;
-  for (const auto& cl : plan->classes) {
+  if (workspace) {  // caller scratch (xft_mehler_workspace_bytes): the classes one after another
+    op.hscratch = static_cast<double2*>(workspace);
+    size_t off = 0;
+    for (const auto& cl : plan->classes) {
+      const long long cnt = cl.second;
+      rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan->list + off, op, st)
+                                 : run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, st);
+      if (rc) return rc;
+      off += cnt;
+    }
+    return XFT_OK;
+  }
+  // Size classes are disjoint row sets: each runs on its own internal stream
+  // (forked from and joined back to `st`, so the call stays stream-ordered and
+  // graph-capturable) with its own scratch, and the small in-CTA classes fill
+  // the SMs the four-step classes' short tile kernels leave idle.
+  char* base = static_cast<char*>(stream_scratch(dev, st, all_bytes));
+  if (!base) return XFT_ECUDA;
+  SideStreams& ss = side_streams(dev, st, (int)plan->classes.size());
+  if (!ss.ok) return XFT_ECUDA;
+  std::lock_guard<std::mutex> lock(ss.mu);
+  if (cudaEventRecord(ss.fork, st) != cudaSuccess) return XFT_ECUDA;
+  size_t off = 0, boff = 0;
+  for (size_t c = 0; c < plan->classes.size() && !rc; ++c) {
+    const auto& cl = plan->classes[c];
     const long long cnt = cl.second;
-    rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan->list + off, op, st)
-                               : run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, st,
-                                                  large_scratch);
-    if (rc) break;
+    cudaStream_t sc = ss.st[c];
+    if (cudaStreamWaitEvent(sc, ss.fork, 0) != cudaSuccess) return XFT_ECUDA;
+    if (cl.first <= MAXL_C128) {
+      OpMehler oc = op;
+      oc.hscratch = reinterpret_cast<double2*>(base + boff);
+      boff += hs_bytes;
+      rc = blue<double2>(cl.first, in, out, cnt, plan->list + off, oc, sc);
+    } else {
+      rc = run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, sc, base + boff);
+      boff += 2 * (size_t)cnt * ((size_t)1 << cl.first) * 16;
+    }
     off += cnt;
   }
+  for (size_t c = 0; c < plan->classes.size(); ++c) {  // join (also after an error: keep `st` consistent)
+    if (cudaEventRecord(ss.join[c], ss.st[c]) != cudaSuccess || cudaStreamWaitEvent(st, ss.join[c], 0) != cudaSuccess)
+      return XFT_ECUDA;
+  }
+  (void)large_bytes;
   return rc;
 }
 
