@@ -253,15 +253,7 @@ struct MehlerPlan {
   int maxl = 0;
 };
 
-// internal streams of a Mehler call on caller stream `st` (fork/join events),
-// created once per (device, caller stream) and grown to the class count
-struct SideStreams {
-  std::mutex mu;
-  std::vector<cudaStream_t> st;
-  std::vector<cudaEvent_t> join;
-  cudaEvent_t fork = nullptr;
-  bool ok = true;
-};
+namespace xftb {
 SideStreams& side_streams(int dev, cudaStream_t caller, int count) {
   static std::mutex mu;
   static std::map<std::pair<int, cudaStream_t>, SideStreams*> pool;
@@ -284,6 +276,7 @@ SideStreams& side_streams(int dev, cudaStream_t caller, int count) {
   }
   return *p;
 }
+}  // namespace xftb
 
 // grown on demand (outside capture: the bench and first calls size it), never shrunk
 void* stream_scratch(int dev, cudaStream_t st, size_t bytes) {

@@ -15,6 +15,9 @@
 
 using namespace xftb;
 
+#ifndef XFT_LCT2D_LANES
+#define XFT_LCT2D_LANES 4  // internal streams for the 8 slab column passes (1 = in order on the caller stream)
+#endif
 #ifndef XFT_LCT2D_SLABS
 #define XFT_LCT2D_SLABS 1  // single-GPU 2-D: row pass into 8 column slabs, cluster columns slab -> natural
 #endif
@@ -379,17 +382,31 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
     const int segl = log2_exact(nc);
     rc = run_rows(MODE_LCT, -1, in, workspace, n_rows, n_cols, dtype, nullptr, 0, ur, 0, st, segl, n_rows * nc);
     if (rc) return rc;
+    // the 8 slabs are independent: two internal streams (forked from / joined to
+    // `st`) so one slab's column kernel starts on the SMs another's tail frees
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SideStreams& ss = side_streams(dev, st, XFT_LCT2D_LANES);
+    if (!ss.ok) return XFT_ECUDA;
+    std::lock_guard<std::mutex> lock(ss.mu);
+    if (cudaEventRecord(ss.fork, st) != cudaSuccess) return XFT_ECUDA;
+    for (int q = 0; q < XFT_LCT2D_LANES; ++q)
+      if (cudaStreamWaitEvent(ss.st[q], ss.fork, 0) != cudaSuccess) return XFT_ECUDA;
     for (int h = 0; h < 8 && !rc; ++h) {
+      cudaStream_t sh = ss.st[h % XFT_LCT2D_LANES];
       const char* slab = static_cast<const char*>(workspace) + esz * (size_t)h * n_rows * nc;
       char* dst = static_cast<char*>(out) + esz * (size_t)h * nc;
-      rc = run_lct_cols_cluster(slab, dst, n_rows, nc, nc, n_cols, dtype, abcd_col, 0, st);
+      rc = run_lct_cols_cluster(slab, dst, n_rows, nc, nc, n_cols, dtype, abcd_col, 0, sh);
       if (rc == XFT_ENOTSUP) {  // no cluster path here: columns in place on the slab, then place it
-        rc = run_lct_cols(slab, const_cast<char*>(slab), nullptr, n_rows, nc, nc, dtype, abcd_col, 0, st);
+        rc = run_lct_cols(slab, const_cast<char*>(slab), nullptr, n_rows, nc, nc, dtype, abcd_col, 0, sh);
         if (!rc && cudaMemcpy2DAsync(dst, esz * n_cols, slab, esz * nc, esz * nc, n_rows, cudaMemcpyDeviceToDevice,
-                                     st) != cudaSuccess)
+                                     sh) != cudaSuccess)
           rc = XFT_ECUDA;
       }
     }
+    for (int q = 0; q < XFT_LCT2D_LANES; ++q)
+      if (cudaEventRecord(ss.join[q], ss.st[q]) != cudaSuccess || cudaStreamWaitEvent(st, ss.join[q], 0) != cudaSuccess)
+        return XFT_ECUDA;
     return rc;
   }
   // axis 1: rows (in -> out); axis 0: columns in place on `out` (workspace = four-step scratch)

@@ -3,9 +3,24 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <vector>
+
 namespace xftb {
 
 struct Abcd;
+
+// internal streams of a call on caller stream `caller` (fork/join events),
+// created once per (device, caller stream) and grown to `count`; independent
+// pieces of one call run concurrently and are joined back before it returns
+struct SideStreams {
+  std::mutex mu;
+  std::vector<cudaStream_t> st;
+  std::vector<cudaEvent_t> join;
+  cudaEvent_t fork = nullptr;
+  bool ok = true;
+};
+SideStreams& side_streams(int dev, cudaStream_t caller, int count);
 
 // chirp-z route for lengths that are not powers of two (xft_bluestein.cu);
 // mode: 0 DFT (sign), 1 scaled Fourier, 2 LCT.  abcd: device, stride 0|4.
