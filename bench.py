@@ -332,7 +332,10 @@ def run_ours(args, rank, world, local_rank):
             return run
         graphs = {}
         per_set = [[(work[k], sets[i][k]) for k in idx] for i in range(nsets)]
-        lanes = [torch.cuda.Stream(dev) for _ in idx]
+        # --lane-priority: the heaviest item's lane (the c128 batch) gets the higher priority, so
+        # freed SM slots go to it first and the lighter batch fills what remains
+        heavy = max(idx, key=lambda k: work[k].values.itemsize) if len(idx) > 1 else None
+        lanes = [torch.cuda.Stream(dev, priority=(-1 if (args.lane_priority and k == heavy) else 0)) for k in idx]
 
         def graph(reps):
             if reps not in graphs:
@@ -345,14 +348,19 @@ def run_ours(args, rank, world, local_rank):
                 with torch.cuda.graph(g, stream=stream):
                     if len(idx) > 1 and args.overlap:
                         # the step's batches are independent: each item's launches are chained
-                        # on its own stream (fork/join around the whole graph), so one batch's
-                        # kernel can start on the SMs another's tail leaves idle
+                        # on its own stream (fork/join around the whole graph, or around every
+                        # step with --overlap 2), so the batches share the SMs
                         for lane in lanes:
                             lane.wait_stream(stream)
                         for r in range(reps):
                             for lane, (it, st) in zip(lanes, per_set[r % nsets]):
                                 with torch.cuda.stream(lane):
                                     launch(it, st)
+                            if args.overlap == 2:
+                                for lane in lanes:
+                                    stream.wait_stream(lane)
+                                for lane in lanes:
+                                    lane.wait_stream(stream)
                         for lane in lanes:
                             stream.wait_stream(lane)
                     else:
@@ -520,6 +528,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: the step's independent batches (c64, c128) on their own streams inside the graph")
+    ap.add_argument("--lane-priority", type=int, default=0, help="1: higher stream priority for the c128 lane")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="cfg5 under torchrun: row-kernel NVLink peer stores (p2p) or NCCL all_to_all")
     args = ap.parse_args()
