@@ -472,6 +472,8 @@ def run_ours(args, rank, world, local_rank):
     roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
             "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"{kname} {dom}",
             "peak_source": peak_kind,
+            "measured": "each kernel alone: K graph-replayed launches on its stream, CUDA events; "
+                        "step_achieved = all items' algorithmic bytes / step time (items on their own streams)",
             "step_achieved": bytes_of(work) / (ms_per_step * 1e-3) / 1e9}
 
     cpu = None
