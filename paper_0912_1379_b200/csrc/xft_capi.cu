@@ -129,8 +129,9 @@ int launch_pipe(const LaunchArgs& a) {
   }
   const long long tiles = (a.batch + Cfg::ROWS - 1) / Cfg::ROWS;
   long long cap = occ;
-#ifdef XFT_GRID_CAP_ENV  // tuning only: XFT_GRID_CAP=<ctas> caps the persistent grid
+#ifdef XFT_GRID_CAP_ENV  // tuning only: XFT_GRID_CAP[64|128]=<ctas> caps the persistent grid
   if (const char* e = getenv("XFT_GRID_CAP")) cap = atoll(e) < cap ? atoll(e) : cap;
+  if (const char* e = getenv(sizeof(C) == 8 ? "XFT_GRID_CAP64" : "XFT_GRID_CAP128")) cap = atoll(e) < cap ? atoll(e) : cap;
 #endif
   const long long grid = tiles < cap ? tiles : cap;
   RowConst kc;
