@@ -86,7 +86,9 @@ struct PipeShape {
   // c64 rows up to 1024: two resident CTAs with a 3-deep ring measured best (cfg4); longer rows: 4 CTAs
   static constexpr int MINB0 = C64 ? (L <= 10 ? 2 : XFT_C64_MINB) : XFT_C128_MINB;
   static constexpr size_t TILE_BYTES = size_t(ROWS) * ((size_t(1) << L) + (size_t(1) << L) / 16) * sizeof(C);
-  static constexpr size_t STATIC = (ROWS >= 128 ? ROWS : 128) * (C64 ? sizeof(Coef64) : sizeof(Coef128)) + 256;
+  static constexpr size_t STATIC =
+      (C64 ? (ROWS >= 128 ? ROWS : 128) * sizeof(Coef64)
+           : (ROWS == 1 ? XFT_C128_CH : (ROWS >= 128 ? ROWS : 128)) * sizeof(Coef128)) + 256;
   static constexpr size_t TAB = C64 ? 0 : XFT_C128_TABCOPIES * C128_TABN * 16;
   // resident CTAs per SM: requested, capped by threads (2048/SM) and by one stage of smem
   static constexpr int MINB_T = 65536 / (TR * ROWS * 64);  // keep >= 64 registers per thread

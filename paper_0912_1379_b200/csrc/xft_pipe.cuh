@@ -66,6 +66,9 @@
 #ifndef XFT_TWGEN
 #define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
 #endif
+#ifndef XFT_C128_CH
+#define XFT_C128_CH 32  // coefficient chunk (rows) of the single-row c128 CTAs
+#endif
 #ifndef XFT_MIRROR
 #define XFT_MIRROR 1  // mirror lane map + shared rounding corrections (see PipeCfg::MIRROR)
 #endif
@@ -949,7 +952,8 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   __shared__ __align__(8) uint64_t bars[S];
   // per-row coefficients of the next CH tiles of this CTA, computed by all
   // threads together once per CH tiles (one make_coef latency per chunk)
-  constexpr int CH = Cfg::MODE == MODE_LCT ? (ROWS >= 128 ? 1 : 128 / ROWS < 32 ? 128 / ROWS : 32) : 1;
+  constexpr int CH = Cfg::MODE == MODE_LCT ? (Cfg::C128 && ROWS == 1 ? XFT_C128_CH
+                                             : ROWS >= 128 ? 1 : 128 / ROWS < 32 ? 128 / ROWS : 32) : 1;
   __shared__ Coef coeft[CH][Cfg::MODE == MODE_LCT ? ROWS : 1];
 
   C* stage0 = reinterpret_cast<C*>(xft_smem);
