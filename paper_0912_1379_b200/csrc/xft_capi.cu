@@ -7,6 +7,7 @@
 #include <mutex>
 #include <cstring>
 #include <utility>
+#include <vector>
 
 #include "../../include/xft_b200.h"
 #include "xft_pipe.cuh"
@@ -290,13 +291,24 @@ struct HostPipe {
     return XFT_OK;
   }
 };
-HostPipe& host_pipe(int dev) {
+// a pool of pipelines per device: concurrent host-buffer calls (e.g. a c64 and
+// a c128 batch from two threads) each take their own streams and staging, so
+// their PCIe transfers interleave instead of queueing behind one lock
+struct PipeLease {
+  HostPipe* p;
+  std::unique_lock<std::mutex> lock;
+};
+PipeLease host_pipe(int dev) {
   static std::mutex m;
-  static std::map<int, HostPipe*> pipes;
-  std::lock_guard<std::mutex> lock(m);
-  HostPipe*& p = pipes[dev];
-  if (!p) p = new HostPipe();
-  return *p;
+  static std::map<int, std::vector<HostPipe*>> pools;
+  std::lock_guard<std::mutex> guard(m);
+  auto& pool = pools[dev];
+  for (HostPipe* p : pool) {
+    std::unique_lock<std::mutex> l(p->mu, std::try_to_lock);
+    if (l.owns_lock()) return PipeLease{p, std::move(l)};
+  }
+  pool.push_back(new HostPipe());
+  return PipeLease{pool.back(), std::unique_lock<std::mutex>(pool.back()->mu)};
 }
 }  // namespace
 
@@ -487,8 +499,8 @@ int xft_lct_host(const void* in, void* out, int64_t batch, int64_t n, int dtype,
   if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
   // per-device persistent streams and staging buffers (grown on demand, never
   // freed): no allocation, stream creation or pool trimming inside the call
-  HostPipe& hp = host_pipe(dev);
-  std::lock_guard<std::mutex> lock(hp.mu);
+  PipeLease lease = host_pipe(dev);  // held for the call
+  HostPipe& hp = *lease.p;
   rc = hp.reserve(row_bytes * (size_t)chunk, abcd_stride ? sizeof(double) * abcd_stride * (size_t)chunk : 0);
   if (rc) return rc;
   const Abcd uni = abcd_stride ? Abcd{0, 0, 0, 0} : Abcd{abcd[0], abcd[1], abcd[2], abcd[3]};
