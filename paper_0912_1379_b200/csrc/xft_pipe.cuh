@@ -66,6 +66,9 @@
 #ifndef XFT_TWGEN
 #define XFT_TWGEN 1  // LCT-mode inter-pass twiddles generated from two table entries per butterfly (0: all loaded)
 #endif
+#ifndef XFT_COEF_PREFETCH
+#define XFT_COEF_PREFETCH 1  // prefetch the first coefficient chunk's parameter rows at kernel entry
+#endif
 #ifndef XFT_C128_CH
 #define XFT_C128_CH 32  // coefficient chunk (rows) of the single-row c128 CTAs
 #endif
@@ -1000,6 +1003,13 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   };
 
   // ---- prologue ----
+  if constexpr (Cfg::MODE == MODE_LCT && XFT_COEF_PREFETCH) {
+    // the first chunk's parameter rows: their global latency overlaps the table copy
+    if (abcd && tid < CH * ROWS) {
+      const long long row = ((long long)blockIdx.x + (long long)(tid / ROWS) * G) * ROWS + tid % ROWS;
+      if (row < batch) asm volatile("prefetch.global.L1 [%0];" ::"l"(abcd + row * abcd_stride));
+    }
+  }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], SPLIT ? 2 : 1);  // split: one arrival per part
     fence_mbar_init();
