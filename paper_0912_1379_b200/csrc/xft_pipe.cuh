@@ -69,6 +69,9 @@
 #ifndef XFT_COEF_PREFETCH
 #define XFT_COEF_PREFETCH 1  // prefetch the first coefficient chunk's parameter rows at kernel entry
 #endif
+#ifndef XFT_TW_PREFETCH
+#define XFT_TW_PREFETCH 0  // (A/B: slower, off) prefetch this thread's first-row twiddle entries at kernel entry
+#endif
 #ifndef XFT_C128_CH
 #define XFT_C128_CH 32  // coefficient chunk (rows) of the single-row c128 CTAs
 #endif
@@ -1008,6 +1011,15 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     if (abcd && tid < CH * ROWS) {
       const long long row = ((long long)blockIdx.x + (long long)(tid / ROWS) * G) * ROWS + tid % ROWS;
       if (row < batch) asm volatile("prefetch.global.L1 [%0];" ::"l"(abcd + row * abcd_stride));
+    }
+  }
+  if constexpr (XFT_TW_PREFETCH && Cfg::NPASS > 1) {
+    // this thread's first-row twiddle entries (w and w^8 of every pass) into L1
+#pragma unroll
+    for (int p = 1; p < Cfg::NPASS; ++p) {
+      const typename Cfg::C* tp = tw + Cfg::twoff(p) + (j & (Cfg::ns(p) - 1));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+      if (Cfg::E >= 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + 7 * Cfg::ns(p)));
     }
   }
   if (tid == 0) {
