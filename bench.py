@@ -6,22 +6,31 @@ transformed in complex64 AND in complex128 (metric "batched LCT Msamples/s at
 N=4096 c64/c128").  `value` is whole-job throughput with inputs resident in
 HBM (CUDA events on the launching stream, max over ranks); `e2e` is the same
 metric through the public host-buffer API (ops.lct_host -> xft_lct_host:
-pinned host in, H2D + kernel + D2H, host out).
+pinned host in, H2D + kernel + D2H, host out).  The default line also carries
+`configs`: configs 1, 3, 4 and 5 measured the same way (GPU value, kernel
+times, roofline fraction, ncu traffic, CPU reference baseline).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg4|...]
-  python bench.py --impl reference ...   # CPU reference path (oracle port), rank 0 only
+  python bench.py --impl reference ...   # the reference's own CPU path, rank 0 only
 
-Multi-GPU (torchrun): rows are independent, so every rank transforms its own
-full batch with no collective (weak scaling); value = N x per-rank samples /
-max-over-ranks time.
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+`torch.distributed.run` with N ranks.  Rows are independent,
+so configs 2/3/4 are STRONG-scaled: rank r transforms rows [rB/N, (r+1)B/N)
+of the one seeded batch, no collective; `weak_scaling` adds the per-rank
+full-batch figure.  Config 5 shards rows and exchanges once (row-kernel
+NVLink peer stores into symmetric memory, NCCL all_to_all fallback).
+
+CPU arms (oracle/cpu_ref.py): the reference package itself, installed into
+oracle/_ref by oracle/build_ref.sh, one fast_lct/fast_frft call per row in a
+process pool fed through shared memory (1-core and P-core figures).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
+import subprocess
 import sys
 import time
 
@@ -31,18 +40,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FALLBACK_HBM_GBS = 6650.0
+METRIC = "batched LCT Msamples/s at N=4096 c64/c128"
+EXTRA_CONFIGS = ("cfg1", "cfg3", "cfg4", "cfg5")
 
 
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback"
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic():
+def load_profile_table():
+    """ncu-derived per-launch DRAM traffic and FP64 op counts (profiles/ncu_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f)
@@ -125,28 +137,45 @@ class ClockSampler:
 # workloads: each item is one transform launched once per step
 # ---------------------------------------------------------------------------
 class Item:
-    """tag, host input, parameters, kind in {lct, mehler, lct2d}; alg_bytes = HBM bytes the op must move."""
+    """tag, host input, parameters, kind in {lct, mehler, lct2d}; alg_bytes = HBM bytes the op must move.
 
-    def __init__(self, tag, kind, values, params, samples=None, alg_bytes=None, extra=None):
+    ``ref`` holds what the CPU reference arm needs (per-row FrFT angles, z, ...)."""
+
+    def __init__(self, tag, kind, values, params, samples=None, alg_bytes=None, extra=None, ref=None):
         self.tag, self.kind, self.values, self.params = tag, kind, values, params
         self.samples = values.size if samples is None else samples
         self.alg_bytes = values.nbytes * 2 if alg_bytes is None else alg_bytes
         self.extra = extra or {}
+        self.ref = ref or {}
 
 
-def make_workload(name: str, rows_override=None, rank=0, world=1):
+def shard(total: int, rank: int, world: int):
+    """Contiguous row block of rank ``rank`` (strong scaling of a fixed batch)."""
+    return total * rank // world, total * (rank + 1) // world
+
+
+def make_workload(name: str, rows_override=None, rank=0, world=1, replicate=False):
+    """The config's items for this rank: rows [rB/W, (r+1)B/W) of the seeded batch (or all of it
+    with ``replicate``, the weak-scaling figure).  cfg5 always shards rows (one exchange)."""
     from paper_0912_1379_b200 import workloads as W
+
+    def rows_of(total):
+        return (0, total) if replicate else shard(total, rank, world)
 
     if name == "cfg2":
         rows = rows_override or 4096
+        s, e = rows_of(rows)
         c64 = W.config2(rows=rows, n=4096, dtype=np.complex64)
         c128 = W.config2(rows=rows, n=4096, dtype=np.complex128)
-        return [Item("c64", "lct", c64.values, c64.abcd), Item("c128", "lct", c128.values, c128.abcd)], \
+        alpha = c64.extra["alpha"][s:e]
+        return [Item("c64", "lct", c64.values[s:e], c64.abcd[s:e], ref={"alpha": alpha}),
+                Item("c128", "lct", c128.values[s:e], c128.abcd[s:e], ref={"alpha": alpha})], \
             {"workload": f"cfg2 batched FrFT {rows}x4096 c64+c128, per-row alpha~U(0,pi) seed 1",
              "rows": rows, "n": 4096}
     if name == "cfg4":
         c4 = W.config4(rows=rows_override or 65536)
-        return [Item("c64", "lct", c4.values, c4.abcd)], \
+        s, e = rows_of(c4.values.shape[0])
+        return [Item("c64", "lct", c4.values[s:e], c4.abcd)], \
             {"workload": f"cfg4 Fourier (0,1,-1,0) {c4.values.shape[0]}x1024 c64, Hermite mixtures seed 3",
              "rows": c4.values.shape[0], "n": 1024}
     if name == "cfg1":
@@ -155,7 +184,9 @@ def make_workload(name: str, rows_override=None, rank=0, world=1):
                                                            "rows": 1, "n": 1024}
     if name == "cfg3":
         c3 = W.config3(rows=rows_override or 1024)
-        return [Item("c128", "mehler", c3.values, c3.extra["z"])], \
+        s, e = rows_of(c3.values.shape[0])
+        z = c3.extra["z"][s:e]
+        return [Item("c128", "mehler", c3.values[s:e], z, ref={"z": z})], \
             {"workload": f"cfg3 complex-z Mehler FrFT {c3.values.shape[0]}x16384 c128, r~U(.5,.99) seed 2",
              "rows": c3.values.shape[0], "n": 16384}
     if name == "cfg5":
@@ -179,90 +210,110 @@ def bytes_of(work):
     return sum(it.alg_bytes for it in work)
 
 
-# ---------------------------------------------------------------------------
-# CPU reference (oracle port) timing
-# ---------------------------------------------------------------------------
-def _cpu_worker(args):
-    kind, p, vals = args
-    from oracle import xft_oracle
-
-    t0 = time.perf_counter()
-    if kind == "mehler":  # the reference's only CPU path: the dense kernel matrix apply (512 outputs per row)
-        for z, f in zip(p, vals):
-            xft_oracle.mehler_apply(z, f.astype(np.complex128), rows_out=np.arange(0, f.shape[0], f.shape[0] // 512),
-                                    chunk=128)
-    else:  # 1-D rows (the 2-D transform is rows then columns of the same kernel)
-        xft_oracle.fast_lct_rows(p, vals.astype(np.complex128))
-    return time.perf_counter() - t0
-
-
-def cpu_reference(work, sample_rows: int, procs: int, pool=None):
-    """Oracle port of the reference fast_lct over a bounded row sample, process pool of `procs`."""
-    from concurrent.futures import ProcessPoolExecutor
-
-    tasks = []
-    total = 0
-    for it in work:
-        v, p = it.values, np.asarray(it.params)
-        rows = min(sample_rows if it.kind != "mehler" else max(procs, sample_rows // 32), v.shape[0])
-        block = max(1, rows // (procs * 4))
-        for s in range(0, rows, block):
-            e = min(rows, s + block)
-            tasks.append((it.kind, p if p.ndim <= 1 and it.kind != "mehler" else p[s:e], v[s:e]))
-        total += rows * (v.shape[1] if it.kind != "mehler" else 512)
-    ex = pool if pool is not None else ProcessPoolExecutor(procs)
-    try:
-        if pool is None:
-            list(ex.map(_cpu_worker, tasks[:procs]))  # warm the workers (imports)
-        t0 = time.perf_counter()
-        list(ex.map(_cpu_worker, tasks))
-        dt = time.perf_counter() - t0
-    finally:
-        if pool is None:
-            ex.shutdown()
-    return total / dt / 1e6, total, dt
-
-
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    work, cfg = make_workload(args.config, args.rows)
-    from concurrent.futures import ProcessPoolExecutor
-
-    procs = len(os.sched_getaffinity(0))
-    # bounded per-step sample so the whole --steps run stays within a few minutes
-    sample_rows = max(procs, min(args.cpu_rows or 512, 32768 // max(1, args.steps)))
-    vals = []
-    with ProcessPoolExecutor(procs) as pool:
-        for _ in range(max(1, args.warmup)):
-            cpu_reference(work, procs, procs, pool)
-        for _ in range(args.steps):
-            v, total, dt = cpu_reference(work, sample_rows, procs, pool)
-            vals.append(v)
-    value = statistics.median(vals)
-    sample = f"{sample_rows} rows per dtype of {cfg['workload']} ({total} samples/step)"
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "Msamples/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded)",
-        "config": cfg,
-        "cpu_baseline": {"value": value, "unit": "Msamples/s", "cores": procs, "kind": "port", "sample": sample},
-        "e2e": {"value": value, "unit": "Msamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-METRIC = "batched LCT Msamples/s at N=4096 c64/c128"
-
-
 def DTYPE_OF(work):
     return "+".join(sorted({it.tag for it in work}))
 
 
 # ---------------------------------------------------------------------------
+# CPU reference (oracle/cpu_ref.py: the reference package itself, shared-memory process pool)
+# ---------------------------------------------------------------------------
+def _arm_kwargs(it):
+    if it.kind == "mehler":
+        return {"z": it.ref["z"]}
+    return {"params": np.asarray(it.params, dtype=np.float64), "alpha": it.ref.get("alpha")}
+
+
+def cpu_baseline_for(work, target_s=4.0, target_1core_s=2.0):
+    """P-core and 1-core reference figures over bounded samples of every item of the workload."""
+    from oracle import cpu_ref
+
+    parts = [cpu_ref.measure(it.kind, it.values, target_s=target_s, target_1core_s=target_1core_s,
+                             **_arm_kwargs(it)) for it in work]
+    if len(parts) == 1:
+        return parts[0]
+
+    def comb(key):  # the step's items back to back: total samples / total seconds
+        s = sum(p[key]["value"] * p[key]["seconds"] for p in parts)
+        t = sum(p[key]["seconds"] for p in parts)
+        return {"cores": parts[0][key]["cores"], "value": s / t, "rows": [p[key]["rows"] for p in parts],
+                "seconds": t}
+
+    cp, c1 = comb("cores_P"), comb("cores_1")
+    return {"value": cp["value"], "unit": "Msamples/s", "cores": cp["cores"], "kind": parts[0]["kind"],
+            "sample": " | ".join(f"{it.tag}: {p['sample']}" for it, p in zip(work, parts)),
+            "cores_P": cp, "cores_1": c1}
+
+
+def run_reference(args, rank, world):
+    """The reference arm: rank 0 times the reference's own CPU implementation; other ranks exit."""
+    if rank != 0:
+        return
+    from oracle import cpu_ref
+
+    work, cfg = make_workload(args.config, args.rows)
+    procs = cpu_ref.host_threads()
+    arms = []
+    try:
+        for it in work:
+            t_row = max(cpu_ref.per_row_seconds(it.kind, it.values, **_arm_kwargs(it)), 1e-6)
+            # bounded per-step sample: ~2 s of pool time per item, at least one row per process
+            rows = args.cpu_rows or int(max(procs, min(it.values.shape[0], round(2.0 * procs / t_row))))
+            arms.append(cpu_ref.CpuArm(it.kind, it.values, rows, procs, **_arm_kwargs(it)))
+        for _ in range(max(1, args.warmup)):
+            for a in arms:
+                a.run(procs)
+        vals = []
+        for _ in range(args.steps):
+            s = t = 0.0
+            for a in arms:
+                ds, dt = a.run()
+                s, t = s + ds, t + dt
+            vals.append(s / t / 1e6)
+        kind = arms[0].kind_label
+        sample = "; ".join(f"{it.tag}: {a.rows} rows of {it.values.shape[1]} per step" for it, a in zip(work, arms))
+    finally:
+        for a in arms:
+            a.close()
+    value = statistics.median(vals)
+    src = "oracle/_ref (the reference xft package), one fast_lct/fast_frft call per row" if kind == "reference" \
+        else "oracle/xft_oracle.py port (oracle/_ref missing)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Msamples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded)",
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "Msamples/s", "cores": procs, "kind": kind,
+                         "sample": f"{sample}; {src}; {procs}-process pool over shared memory"},
+        "e2e": {"value": value, "unit": "Msamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# FP64 peak probe (tools/libxft_probe.so: a DFMA-chain kernel), for the FP64 roofline
+# ---------------------------------------------------------------------------
+def fp64_peak_tflops(dev_index):
+    import ctypes
+
+    path = os.path.join(ROOT, "tools", "libxft_probe.so")
+    try:
+        lib = ctypes.CDLL(path)
+        lib.xft_probe_fp64_tflops.restype = ctypes.c_double
+        lib.xft_probe_fp64_tflops.argtypes = [ctypes.c_int]
+        v = float(lib.xft_probe_fp64_tflops(dev_index))
+        return v if v > 0 else None
+    except OSError:
+        return None
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def run_ours(args, rank, world, local_rank):
+LAUNCHES = {"lct": 1, "mehler": 14, "lct2d1": 9, "lct2dN": 2}
+
+
+def measure_config(name, args, rank, world, local_rank, steps, replicate=False, e2e=True, clocks=True):
+    """Times `steps` steps of config `name` on this rank; returns the rank-0 record (None elsewhere)."""
     import torch
 
     from paper_0912_1379_b200 import lct2d as L2
@@ -270,12 +321,11 @@ def run_ours(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    work, cfg = make_workload(args.config, args.rows, rank, world)
+    work, cfg = make_workload(name, args.rows if name == args.config else None, rank, world, replicate)
     nsets = 3  # rotate 3 input/output sets: every launch reads cold data (inputs > L2 for cfg2..5)
     stream = torch.cuda.Stream(dev)
 
-    # validate once (reference order) outside the timed region
-    for it in work:
+    for it in work:  # validate once (reference order) outside the timed region
         if it.kind == "lct":
             ops.validate_abcd_host(it.params)
 
@@ -296,6 +346,8 @@ def run_ours(args, rank, world, local_rank):
                            torch.empty((world, rl, n // world), dtype=st.vin.dtype, device=dev))
         return st
 
+    transport = [args.transport]
+
     def launch(it, st):
         """Launches one transform; returns the tensor holding its result."""
         if it.kind == "lct":
@@ -304,22 +356,20 @@ def run_ours(args, rank, world, local_rank):
             return mehler.mehler_rows(st.vin, st.p, out=st.vout)
         elif world == 1:
             return L2.lct2d(st.vin, st.p, st.p, out=st.vout, workspace=st.ws)
-        else:
-            if args.transport == "p2p":
-                try:  # row kernel stores straight into the peers' symmetric-memory slabs
-                    return L2.lct2d_sharded(st.vin, st.p, st.p, transport="p2p")
-                except (RuntimeError, NotImplementedError) as e:
-                    print(f"p2p transport unavailable ({e}); falling back to NCCL all_to_all", file=sys.stderr)
-                    args.transport = "nccl"
-            return L2.lct2d_sharded(st.vin, st.p, st.p, buffers=st.bufs)
+        if transport[0] == "p2p":
+            try:  # row kernel stores straight into the peers' symmetric-memory slabs
+                return L2.lct2d_sharded(st.vin, st.p, st.p, transport="p2p")
+            except (RuntimeError, NotImplementedError) as e:
+                print(f"p2p transport unavailable ({e}); falling back to NCCL all_to_all", file=sys.stderr)
+                transport[0] = "nccl"
+        return L2.lct2d_sharded(st.vin, st.p, st.p, buffers=st.bufs)
 
     sets = [[make_state(it) for it in work] for _ in range(nsets)]
-    # The sharded 2-D pass calls NCCL through torch.distributed: it is launched
-    # directly; everything else (incl. the Mehler path, whose per-row plans are
-    # built and cached on the device by the warm-up call before capture) is
-    # captured as CUDA graphs so the timed loop has no host launch overhead.
+    # The sharded 2-D pass synchronises ranks through torch.distributed: it is launched directly;
+    # everything else (incl. the Mehler path, whose per-row plans are built and cached on the
+    # device by the warm-up call before capture) is captured as CUDA graphs.
     capturable = all(it.kind in ("lct", "mehler") or (it.kind == "lct2d" and world == 1) for it in work)
-    chunk = max(1, min(10, args.steps))
+    chunk = max(1, min(10, steps))
 
     def runner(item_idx):
         """callable(n_steps) that launches n steps on `stream` (all items, or one item)."""
@@ -332,10 +382,7 @@ def run_ours(args, rank, world, local_rank):
             return run
         graphs = {}
         per_set = [[(work[k], sets[i][k]) for k in idx] for i in range(nsets)]
-        # --lane-priority: the heaviest item's lane (the c128 batch) gets the higher priority, so
-        # freed SM slots go to it first and the lighter batch fills what remains
-        heavy = max(idx, key=lambda k: work[k].values.itemsize) if len(idx) > 1 else None
-        lanes = [torch.cuda.Stream(dev, priority=(-1 if (args.lane_priority and k == heavy) else 0)) for k in idx]
+        lanes = [torch.cuda.Stream(dev) for _ in idx]
 
         def graph(reps):
             if reps not in graphs:
@@ -347,20 +394,14 @@ def run_ours(args, rank, world, local_rank):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
                     if len(idx) > 1 and args.overlap:
-                        # the step's batches are independent: each item's launches are chained
-                        # on its own stream (fork/join around the whole graph, or around every
-                        # step with --overlap 2), so the batches share the SMs
+                        # the step's batches are independent: each item's launches are chained on
+                        # its own stream (fork/join around the whole graph): the batches share the SMs
                         for lane in lanes:
                             lane.wait_stream(stream)
                         for r in range(reps):
                             for lane, (it, st) in zip(lanes, per_set[r % nsets]):
                                 with torch.cuda.stream(lane):
                                     launch(it, st)
-                            if args.overlap == 2:
-                                for lane in lanes:
-                                    stream.wait_stream(lane)
-                                for lane in lanes:
-                                    lane.wait_stream(stream)
                         for lane in lanes:
                             stream.wait_stream(lane)
                     else:
@@ -371,8 +412,8 @@ def run_ours(args, rank, world, local_rank):
             return graphs[reps]
 
         graph(chunk)
-        if args.steps % chunk:
-            graph(args.steps % chunk)
+        if steps % chunk:
+            graph(steps % chunk)
 
         def run(nsteps):
             for _ in range(nsteps // chunk):
@@ -397,28 +438,62 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         return e0.elapsed_time(e1)
 
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
     with torch.cuda.stream(stream):
         step_run = runner(None)
-        kern_runs = [runner(k) for k in range(len(work))]
+        kern_runs = [runner(k) for k in range(len(work))] if len(work) > 1 else [step_run]
         step_run(max(args.warmup, 3))  # warm-up (graphs for the remainder are captured here too)
         torch.cuda.synchronize()
-        kern_ms = [timed(kern_runs[k], args.steps) / args.steps for k in range(len(work))]
-        with ClockSampler(local_rank) as clk:
-            total_ms = timed(step_run, args.steps)
+        kern_ms = [max_over_ranks(timed(kern_runs[k], steps)) / steps for k in range(len(work))] \
+            if len(work) > 1 else None
+        if clocks:
+            with ClockSampler(local_rank) as clk:
+                total_ms = timed(step_run, steps)
+        else:
+            clk = None
+            total_ms = timed(step_run, steps)
+    total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / steps
+    if kern_ms is None:
+        kern_ms = [ms_per_step]
+    # whole-job samples: every rank's shard (configs 2-4 strong-scaled: the shards add up to the batch)
+    samples_job = samples_of(work)
     if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    samples = samples_of(work)
-    value = world * samples / (ms_per_step * 1e-3) / 1e6
-    # our kernels per step (ncu launch lists, profiles/r1/final/launches_*.txt): a row batch is one
-    # xft_pipe_kernel; config 3's Mehler step is 2 xft_blue_kernel + 10 xft_tile_kernel + 2 zero-fill
-    # kernels; the single-GPU 2-D step is 1 row kernel + 8 cluster column kernels (one per slab),
-    # the sharded one 1 row kernel + 1 column kernel per rank
-    launches_per_step = sum({"lct": 1, "mehler": 14, "lct2d": 9 if world == 1 else 2}[it.kind] for it in work)
+        t = torch.tensor([float(samples_job)], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        samples_job = int(t.item())
+    value = samples_job / (ms_per_step * 1e-3) / 1e6
+    launches_per_step = sum(LAUNCHES[it.kind if it.kind != "lct2d" else ("lct2d1" if world == 1 else "lct2dN")]
+                            for it in work)
 
-    # end-to-end through the public host-buffer API: pinned host in, result back on the host
+    e2e_rec = None
+    if e2e:
+        e2e_rec = measure_e2e(work, sets, launch, dev, args, world, samples_job, barrier, max_over_ranks)
+
+    rec = {"value": value, "ms_per_step": ms_per_step, "steps": steps, "config": cfg, "work": work,
+           "kern_ms": kern_ms, "samples_job": samples_job, "capturable": capturable,
+           "launches": launches_per_step * steps, "clocks": clk.summary() if clk else None, "e2e": e2e_rec,
+           "transport": transport[0]}
+    del sets
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return rec
+
+
+def measure_e2e(work, sets, launch, dev, args, world, samples_job, barrier, max_over_ranks):
+    """End to end through the public host-buffer API: pinned host in, result back on the host."""
+    import threading
+
+    import torch
+
+    from paper_0912_1379_b200 import ops
+
     e2e_steps = max(2, min(args.steps, args.e2e_steps))
     pinned = []
     for it in work:
@@ -430,12 +505,11 @@ def run_ours(args, rank, world, local_rank):
         if args.overlap and len(pinned) > 1 and all(it.kind == "lct" for it, _, _ in pinned):
             # independent batches from two host threads: each call takes its own host pipeline
             # (streams + staging), so one batch's H2D fills the other's D2H-only drain
-            import threading
-
             errs = []
 
             def one(it, hin, hout):
                 try:
+                    torch.cuda.set_device(dev)  # the CUDA current device is per host thread
                     ops.lct_host(hin.numpy(), it.params, out=hout.numpy())
                 except Exception as e:  # surfaced below
                     errs.append(e)
@@ -464,100 +538,162 @@ def run_ours(args, rank, world, local_rank):
     te = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_once()
-    e2e_dt = time.perf_counter() - te
-    if world > 1:
-        t = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_dt = float(t.item())
-    e2e_value = world * samples * e2e_steps / e2e_dt / 1e6
+    e2e_dt = max_over_ranks(time.perf_counter() - te)
     h2d = sum(h.nbytes for _, h, _ in pinned) + sum(np.asarray(it.params).nbytes for it in work)
     d2h = sum(o.nbytes for _, _, o in pinned)
+    return {"value": samples_job * e2e_steps / e2e_dt / 1e6, "unit": "Msamples/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+            "api": "ops.lct_host -> xft_lct_host" if work[0].kind == "lct" else "pinned H2D + public op + D2H"}
 
-    if rank != 0:
-        return
-    peak, peak_kind = load_peaks()
-    traffic = load_traffic()
+
+FP64_ALG_FLOPS = {  # algorithmic fp64 flops per output sample of a c128 row (5 n log2 n FFT + 2 complex products)
+    "lct": lambda n: 5.0 * np.log2(n) + 12.0,
+    # Mehler rows: 3 length-M FFTs (M ~ 2n windowed) + 3 complex products per sample
+    "mehler": lambda n: 3 * 5.0 * np.log2(2 * n) * 2 + 18.0,
+}
+
+
+def roofline_of(name, rec, world, peak, peak_src, fp64_peak):
+    """Per-item kernel figures and the dominant item's roofline object."""
+    prof = load_profile_table()
+    work = rec["work"]
     per = {}
     for k, it in enumerate(work):
-        ach = it.alg_bytes / (kern_ms[k] * 1e-3) / 1e9
-        per[it.tag] = {"kernel_ms": kern_ms[k], "Msamples_per_s": it.samples / (kern_ms[k] * 1e-3) / 1e6,
+        ms = rec["kern_ms"][k]
+        ach = it.alg_bytes / (ms * 1e-3) / 1e9
+        tr = prof.get(f"{name}_{it.tag}")
+        per[it.tag] = {"kernel_ms": ms, "Msamples_per_s": it.samples / (ms * 1e-3) / 1e6,
                        "achieved_GBps": ach, "frac": ach / peak, "alg_bytes_per_launch": it.alg_bytes,
-                       "traffic": traffic.get(f"{args.config}_{it.tag}")}
+                       "traffic": tr}
+        if it.tag == "c128" and fp64_peak and it.kind in FP64_ALG_FLOPS:
+            n = it.values.shape[1]
+            fl = FP64_ALG_FLOPS[it.kind](n) * it.samples
+            issued = prof.get(f"{name}_{it.tag}_fp64_ops_per_sample")
+            f64 = {"algorithmic_flops_per_launch": fl, "achieved_TFLOPs": fl / (ms * 1e-3) / 1e12,
+                   "peak_TFLOPs": fp64_peak, "frac": fl / (ms * 1e-3) / 1e12 / fp64_peak,
+                   "peak_source": "measured DFMA chain (tools/xft_probe.cu), 2 flops per DFMA"}
+            if issued:  # the FP64 pipe's load: issued fp64 lane-ops (ncu) vs the DFMA lane rate
+                f64["issued_ops_per_sample"] = issued
+                f64["pipe_frac"] = issued * it.samples / (ms * 1e-3) / (fp64_peak * 1e12 / 2)
+            per[it.tag]["fp64"] = f64
         if "nvl_bytes" in it.extra and world > 1:
             t_roof = it.alg_bytes / (peak * 1e9) + it.extra["nvl_bytes"] / 900e9
             per[it.tag]["hbm_nvlink_serial_roofline_ms"] = t_roof * 1e3
-            per[it.tag]["frac_of_hbm_nvlink_roofline"] = t_roof * 1e3 / kern_ms[k]
+            per[it.tag]["frac_of_hbm_nvlink_roofline"] = t_roof * 1e3 / ms
     dom = max(per, key=lambda t: per[t]["kernel_ms"])
+    kind = work[[it.tag for it in work].index(dom)].kind
     kname = {"lct": "xft_pipe_kernel", "mehler": "xft_blue_kernel + xft_tile_kernel",
-             "lct2d": "xft_pipe_kernel + xft_colclu_kernel"}[work[[it.tag for it in work].index(dom)].kind]
+             "lct2d": "xft_pipe_kernel + xft_colclu_kernel"}[kind]
     roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
             "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"{kname} {dom}",
-            "peak_source": peak_kind,
-            "measured": "each kernel alone: K graph-replayed launches on its stream, CUDA events; "
-                        "step_achieved = all items' algorithmic bytes / step time (items on their own streams)",
-            "step_achieved": bytes_of(work) / (ms_per_step * 1e-3) / 1e9}
+            "peak_source": peak_src,
+            "measured": "each item alone: K graph-replayed launches on its stream, CUDA events; "
+                        "step_achieved = all items' algorithmic bytes / step time",
+            "step_achieved": bytes_of(work) / (rec["ms_per_step"] * 1e-3) / 1e9}
+    if "fp64" in per[dom]:
+        roof["fp64"] = per[dom]["fp64"]
+    return per, roof
 
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    peak, peak_src = load_peaks()
+    fp64_peak = fp64_peak_tflops(local_rank) if rank == 0 else None
+    head = measure_config(args.config, args, rank, world, local_rank, args.steps)
+    extras = {}
+    if args.config == "cfg2" and not args.no_extras:
+        for c in EXTRA_CONFIGS:
+            extras[c] = measure_config(c, args, rank, world, local_rank, min(args.steps, args.extra_steps),
+                                       e2e=False, clocks=False)
+    weak = None
+    if world > 1 and args.config in ("cfg2", "cfg3", "cfg4"):
+        weak = measure_config(args.config, args, rank, world, local_rank, min(args.steps, args.extra_steps),
+                              replicate=True, e2e=False, clocks=False)
+    if rank != 0:
+        return
+    work = head["work"]
+    per, roof = roofline_of(args.config, head, world, peak, peak_src, fp64_peak)
     cpu = None
     if world == 1 and not args.no_cpu:
-        from concurrent.futures import ProcessPoolExecutor
-
-        procs = len(os.sched_getaffinity(0))
-        # bounded sample of the same workload: whole rows of every item (the full batch for the 1-D
-        # configs), repeated until >= 10 s of CPU work (core-seconds), at most 4 passes
-        rows = args.cpu_rows or max(it.values.shape[0] for it in work)
-        vals, core_s, passes, total = [], 0.0, 0, 0
-        with ProcessPoolExecutor(procs) as pool:
-            cpu_reference(work, procs, procs, pool)  # warm the workers (imports)
-            while passes < 4 and (core_s < 10.0 or passes == 0):
-                v, total, dt = cpu_reference(work, rows, procs, pool)
-                vals.append(v)
-                core_s += dt * procs
-                passes += 1
-        cpu = {"value": statistics.median(vals), "unit": "Msamples/s", "cores": procs, "kind": "port",
-               "sample": f"{rows} rows per item of the same batch ({total} samples per pass, {passes} passes, "
-                         f"{core_s:.0f} core-s), oracle/xft_oracle.py in a {procs}-process pool"}
+        cpu = cpu_baseline_for(work)
+    cfgs = {}
+    for c, rec in extras.items():
+        p, r = roofline_of(c, rec, world, peak, peak_src, fp64_peak)
+        cfgs[c] = {"workload": rec["config"]["workload"], "value": rec["value"], "unit": "Msamples/s",
+                   "ms_per_step": rec["ms_per_step"], "steps": rec["steps"], "dtype": DTYPE_OF(rec["work"]),
+                   "roofline": r, "per_dtype": p, "gpu_launches": rec["launches"],
+                   "cpu_baseline": (cpu_baseline_for(rec["work"], 3.0, 1.5)
+                                    if world == 1 and not args.no_cpu else None)}
+        if c == "cfg5":
+            cfgs[c]["transport"] = rec["transport"] if world > 1 else "single GPU (rows -> 8 slabs -> columns)"
+    strong = args.config in ("cfg2", "cfg3", "cfg4") and world > 1
     line = {
-        "metric": METRIC, "value": value, "unit": "Msamples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": head["value"], "unit": "Msamples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong" if args.config in ("cfg2", "cfg3", "cfg4") else "weak",
         "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded, BASELINE config draw order)",
-        "config": dict(cfg, l2="3 rotating input/output sets; each launch streams >= 2x L2 of cold data",
-                       parallelism=(f"batch-sharded x{world}, no collective" if args.config != "cfg5"
-                                    else f"row-sharded x{world}, " + ("row-kernel NVLink peer stores (symmetric memory)"
-                                                                     if args.transport == "p2p" and world > 1
-                                                                     else "one NCCL all_to_all_single")),
-                       timing=("CUDA graphs" if capturable else "direct launches")
-                       + (", step items on independent streams" if capturable and args.overlap and len(work) > 1
-                          else "")),
-        "roofline": roof, "per_dtype": per, "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "Msamples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "steps": e2e_steps, "api": "ops.lct_host -> xft_lct_host" if work[0].kind == "lct"
-                else "pinned H2D + public op + D2H"},
-        "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
+        "config": dict(head["config"], l2="3 rotating input/output sets; each launch streams >= 2x L2 of cold data",
+                       parallelism=(f"rows sharded over {world} GPU(s) (rank r: rows [rB/N,(r+1)B/N)), "
+                                    "no collective" if args.config != "cfg5"
+                                    else f"row-sharded x{world}, " + ("row-kernel NVLink peer stores"
+                                                                      if head["transport"] == "p2p" and world > 1
+                                                                      else ("NCCL all_to_all_single" if world > 1
+                                                                            else "single GPU"))),
+                       timing=("CUDA graphs" if head["capturable"] else "direct launches")
+                       + (", step items on independent streams" if head["capturable"] and args.overlap
+                          and len(work) > 1 else "")),
+        "roofline": roof, "per_dtype": per, "cpu_baseline": cpu, "e2e": head["e2e"],
+        "gpu_launches": head["launches"], "clocks": head["clocks"],
     }
+    if cfgs:
+        line["configs"] = cfgs
+    if weak is not None:
+        line["weak_scaling"] = {"value": weak["value"], "unit": "Msamples/s", "ms_per_step": weak["ms_per_step"],
+                                "what": f"every rank transforms the full {args.config} batch (replicated rows)"}
+    if strong:
+        line["config"]["shard_rows_per_rank"] = head["work"][0].values.shape[0]
     print(json.dumps(line), flush=True)
+    del torch
+
+
+def relaunch_under_torchrun(n):
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--rows", type=int, default=None)
-    ap.add_argument("--cpu-rows", type=int, default=None, help="CPU baseline rows per item (default: full batch)")
+    ap.add_argument("--cpu-rows", type=int, default=None, help="reference arm: rows per item per step")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--extra-steps", type=int, default=200, help="steps for the per-config extras")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: the step's independent batches (c64, c128) on their own streams inside the graph")
-    ap.add_argument("--lane-priority", type=int, default=0, help="1: higher stream priority for the c128 lane")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="cfg5 under torchrun: row-kernel NVLink peer stores (p2p) or NCCL all_to_all")
+                    help="cfg5 with N>1: row-kernel NVLink peer stores (p2p) or NCCL all_to_all")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
