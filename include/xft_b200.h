@@ -17,12 +17,28 @@
  * i.e. the memory layout of numpy/torch complex arrays.  Out-of-place; the
  * input is never written (reference contract xft/fftcore.py:113).
  *
+ * Alignment: device (and host) data pointers must be 16-byte aligned (the row
+ * kernels move rows with cp.async.bulk); the Python layer copies misaligned
+ * views to an aligned buffer before calling.
+ *
  * Status codes mirror the reference exception classes (xft/errors.py:4-49).
  * Device entry points are stream-ordered and never synchronise the host;
  * parameters passed through device memory are assumed pre-validated (call
  * xft_validate_lct_params on the host copy, as the Python layer does).
- * All entry points are thread-safe; the only global state is the lazily
- * built, immutable per-(device, n, dtype) twiddle/phase tables.
+ *
+ * Threading (reference contract: xft/fftcore.py:8-11, pkg/tests/test_fftcore.py:
+ * 97-148): all entry points are thread-safe and reentrant; identical inputs give
+ * bit-identical outputs on any thread.  Global state, all behind locks:
+ *   - immutable per-(device, n, dtype) twiddle/phase tables and chirp-z plans,
+ *     built once on first use and kept for the process lifetime;
+ *   - the implicit Mehler plan cache of xft_mehler (exact-z keyed, LRU of 64;
+ *     evicted plans are retired, not freed) and per-(device, stream) scratch
+ *     (growth retires the old buffer).  Retired memory may still be referenced
+ *     by a CUDA graph captured earlier, so it is released only by
+ *     xft_release_caches().  Callers that capture graphs around xft_mehler can
+ *     instead own their plan (xft_mehler_plan_create / _destroy).
+ * CUDA-graph capture: every device entry point is capturable once its tables
+ * exist (call it once, or xft_prepare, before capture).
  */
 #ifndef XFT_B200_H
 #define XFT_B200_H
@@ -116,6 +132,23 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
                void* workspace, void* stream);
 /* Host check of z values (FrftOrder / mehler_kernel, xft/dense.py:49-59, 127-130). */
 int xft_validate_mehler_z(const double* z, int64_t count, int64_t stride, int64_t* bad_row);
+
+/* Caller-owned Mehler plan for one z array on the current device (the
+ * analogue of holding frft_matrix_asymptotic's DenseTransform,
+ * xft/dense.py:139-151): per-row parameters, size classes and row lists,
+ * built once (validated like xft_mehler).  xft_mehler_planned applies it to a
+ * [batch][n] complex128 batch (workspace as xft_mehler).  A plan is immutable and
+ * may be used from several threads/streams at once; destroy it only when no
+ * pending work or live CUDA graph uses it. */
+int xft_mehler_plan_create(int64_t batch, int64_t n, const double* z, int64_t z_stride, void** plan);
+int xft_mehler_planned(const void* in, void* out, const void* plan, void* workspace, void* stream);
+int xft_mehler_plan_destroy(void* plan);
+
+/* Releases the implicit Mehler plan cache, retired plans and the internal
+ * per-stream scratch buffers.  The caller guarantees that no pending work and
+ * no live CUDA graph references them (e.g. after cudaDeviceSynchronize and
+ * destroying graphs captured around xft_mehler / xft_lct2d). */
+int xft_release_caches(void);
 
 /* Separable 2-D LCT on one device: fast LCT along rows (abcd_row, host) then
  * along columns (abcd_col, host) of an n_rows x n_cols field (device in/out).

@@ -14,7 +14,7 @@ import threading
 from .errors import XftError, raise_for
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("XFT_LIB") or os.path.join(_HERE, "libxft_b200.so")  # XFT_LIB: tuning builds only
+LIB_PATH = os.path.join(_HERE, "libxft_b200.so")
 
 C64 = 0
 C128 = 1
@@ -45,6 +45,10 @@ _SIGS = {
     "xft_mehler_workspace_bytes": ([_i64, _i64], _i64),
     "xft_mehler": ([_vp, _vp, _i64, _i64, _vp, _i64, _vp, _vp], ctypes.c_int),
     "xft_validate_mehler_z": ([_vp, _i64, _i64, ctypes.POINTER(_i64)], ctypes.c_int),
+    "xft_mehler_plan_create": ([_i64, _i64, _vp, _i64, ctypes.POINTER(_vp)], ctypes.c_int),
+    "xft_mehler_planned": ([_vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "xft_mehler_plan_destroy": ([_vp], ctypes.c_int),
+    "xft_release_caches": ([], ctypes.c_int),
     "xft_lct2d": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp], ctypes.c_int),
     "xft_transpose": ([_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
     "xft_lct_columns": ([_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <complex>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <tuple>
 #include <utility>
@@ -246,11 +247,27 @@ MehlerPlanRow mehler_row(std::complex<double> z, int64_t n) {
 // z array (the B200 analogue of frft_matrix_asymptotic's DenseTransform,
 // xft/dense.py:139-151), built on the host once and kept on the device.  Calls
 // with the same (n, z) reuse it: no host work, no copies, no synchronisation.
+// Immutable once built; shared (refcounted) between the implicit cache and
+// every call using it.  It also keeps the exact z values it was built from, so
+// a cache hit is an exact match, never a hash match.
 struct MehlerPlan {
+  int dev = 0;
+  int64_t batch = 0, n = 0;
+  std::vector<double> z;                    // [batch][2] as used (z_stride 0 -> one row repeated)
   OpMehlerRow* rows = nullptr;              // [batch] device
   int* list = nullptr;                      // [batch] device, rows grouped by class
   std::vector<std::pair<int, long long>> classes;  // (log2 M, count) in list order
   int maxl = 0;
+  ~MehlerPlan() {
+    if (rows || list) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(dev);
+      cudaFree(rows);
+      cudaFree(list);
+      cudaSetDevice(cur);
+    }
+  }
 };
 
 namespace xftb {
@@ -278,85 +295,233 @@ SideStreams& side_streams(int dev, cudaStream_t caller, int count) {
 }
 }  // namespace xftb
 
-// grown on demand (outside capture: the bench and first calls size it), never shrunk
-void* stream_scratch(int dev, cudaStream_t st, size_t bytes) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> pool;
-  std::lock_guard<std::mutex> lock(mu);
-  auto& e = pool[{dev, st}];
-  if (e.second < bytes) {
-    if (e.first) {
-      if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
-      cudaFree(e.first);
-      e.first = nullptr;
+namespace {
+// Runs `f` with this thread's stream-capture mode relaxed, so plan/scratch
+// allocation (cudaMalloc, a pageable cudaMemcpy) is legal while the caller's
+// stream is being captured into a CUDA graph; the mode is restored after.
+template <class F>
+auto relaxed_capture(F&& f) {
+  cudaStreamCaptureMode m = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&m);
+  auto r = f();
+  cudaThreadExchangeStreamCaptureMode(&m);
+  return r;
+}
+
+// Device memory that graphs captured earlier may still reference is never
+// freed implicitly: superseded scratch buffers and evicted plans are retired
+// here and released only by xft_release_caches() (the caller's promise that no
+// pending work or live graph uses them).
+struct Retired {
+  std::mutex mu;
+  std::vector<std::pair<int, void*>> buffers;
+  std::vector<std::shared_ptr<const MehlerPlan>> plans;
+};
+Retired& retired() {
+  static Retired* r = new Retired();  // leaked on purpose: outlives static destruction order
+  return *r;
+}
+
+struct ScratchPool {
+  std::mutex mu;
+  std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> pool;
+};
+ScratchPool& scratch_pool() {
+  static ScratchPool* p = new ScratchPool();
+  return *p;
+}
+
+struct PlanCache {
+  std::mutex mu;
+  // (device, batch, n, FNV-1a of z) -> plans with that key (exact z compared on lookup)
+  std::map<std::tuple<int, int64_t, int64_t, uint64_t>, std::vector<std::shared_ptr<const MehlerPlan>>> map;
+  std::vector<std::shared_ptr<const MehlerPlan>> lru;  // most recently used last
+};
+PlanCache& plan_cache() {
+  static PlanCache* c = new PlanCache();
+  return *c;
+}
+constexpr size_t PLAN_CACHE_ENTRIES = 64;
+
+std::vector<double> gather_z(int64_t batch, const double* z, int64_t z_stride) {
+  std::vector<double> v(2 * batch);
+  for (int64_t r = 0; r < batch; ++r) {
+    const double* zz = z + (z_stride ? r * z_stride : 0);
+    v[2 * r] = zz[0];
+    v[2 * r + 1] = zz[1];
+  }
+  return v;
+}
+
+uint64_t fnv1a(const std::vector<double>& v) {
+  uint64_t h = 1469598103934665603ull;
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(v.data());
+  for (size_t i = 0; i < v.size() * sizeof(double); ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h;
+}
+
+// builds a plan for the (already validated) z values on device `dev`
+int build_mehler_plan(int dev, int64_t batch, int64_t n, std::vector<double> zv,
+                      std::shared_ptr<const MehlerPlan>* out) {
+  auto p = std::make_shared<MehlerPlan>();
+  p->dev = dev;
+  p->batch = batch;
+  p->n = n;
+  std::vector<OpMehlerRow> rows(batch);
+  std::map<int, std::vector<int>> classes;
+  for (int64_t r = 0; r < batch; ++r) {
+    const MehlerPlanRow pr = mehler_row(std::complex<double>(zv[2 * r], zv[2 * r + 1]), n);
+    rows[r] = pr.p;
+    classes[pr.l].push_back((int)r);
+  }
+  std::vector<int> list;
+  list.reserve(batch);
+  for (auto& kv : classes) {
+    list.insert(list.end(), kv.second.begin(), kv.second.end());
+    p->classes.emplace_back(kv.first, (long long)kv.second.size());
+    if (kv.first <= MAXL_C128) p->maxl = kv.first;
+  }
+  p->z = std::move(zv);
+  const bool ok = relaxed_capture([&]() {
+    return cudaMalloc(&p->rows, batch * sizeof(OpMehlerRow)) == cudaSuccess &&
+           cudaMalloc(&p->list, batch * sizeof(int)) == cudaSuccess &&
+           cudaMemcpy(p->rows, rows.data(), batch * sizeof(OpMehlerRow), cudaMemcpyHostToDevice) == cudaSuccess &&
+           cudaMemcpy(p->list, list.data(), batch * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+  });
+  if (!ok) {
+    cudaGetLastError();
+    return XFT_ECUDA;  // ~MehlerPlan frees what was allocated
+  }
+  *out = std::move(p);
+  return XFT_OK;
+}
+
+// the implicit per-process cache behind xft_mehler: exact-z lookup, bounded LRU;
+// evicted plans are retired (not freed), so graphs captured with them stay valid
+int cached_mehler_plan(int dev, int64_t batch, int64_t n, const double* z, int64_t z_stride,
+                       std::shared_ptr<const MehlerPlan>* out) {
+  std::vector<double> zv = gather_z(batch, z, z_stride);
+  const auto key = std::make_tuple(dev, batch, n, fnv1a(zv));
+  PlanCache& c = plan_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  for (const auto& p : c.map[key]) {
+    if (p->z == zv) {  // exact match of every value (a hash collision cannot alias two z arrays)
+      auto pos = std::find(c.lru.begin(), c.lru.end(), p);
+      if (pos != c.lru.end()) std::rotate(pos, pos + 1, c.lru.end());
+      *out = p;
+      return XFT_OK;
     }
-    if (cudaMalloc(&e.first, bytes) != cudaSuccess) {
-      e.first = nullptr;
-      e.second = 0;
+  }
+  std::shared_ptr<const MehlerPlan> p;
+  int rc = build_mehler_plan(dev, batch, n, std::move(zv), &p);
+  if (rc) return rc;
+  if (c.lru.size() >= PLAN_CACHE_ENTRIES) {
+    std::shared_ptr<const MehlerPlan> old = c.lru.front();
+    c.lru.erase(c.lru.begin());
+    auto& bucket = c.map[std::make_tuple(old->dev, old->batch, old->n, fnv1a(old->z))];
+    bucket.erase(std::remove(bucket.begin(), bucket.end(), old), bucket.end());
+    std::lock_guard<std::mutex> rl(retired().mu);
+    retired().plans.push_back(std::move(old));
+  }
+  c.map[key].push_back(p);
+  c.lru.push_back(p);
+  *out = std::move(p);
+  return XFT_OK;
+}
+}  // namespace
+
+// Per-(device, stream) scratch, grown on demand and never shrunk.  Growth
+// allocates a new buffer and retires the old one (work already queued, or a
+// graph captured earlier, may still use it): no synchronisation, legal during
+// stream capture.
+void* xftb::stream_scratch(int dev, cudaStream_t st, size_t bytes) {
+  ScratchPool& sp = scratch_pool();
+  std::lock_guard<std::mutex> lock(sp.mu);
+  auto& e = sp.pool[{dev, st}];
+  if (e.second < bytes) {
+    void* p = nullptr;
+    if (!relaxed_capture([&]() { return cudaMalloc(&p, bytes) == cudaSuccess; })) {
+      cudaGetLastError();
       return nullptr;
     }
+    if (e.first) {
+      std::lock_guard<std::mutex> rl(retired().mu);
+      retired().buffers.emplace_back(dev, e.first);
+    }
+    e.first = p;
     e.second = bytes;
   }
   return e.first;
 }
 
-int mehler_plan(int dev, int64_t batch, int64_t n, const double* z, int64_t z_stride, const MehlerPlan** out) {
-  static std::mutex mu;
-  static std::map<std::tuple<int, int64_t, int64_t, uint64_t>, MehlerPlan> cache;
-  static std::vector<std::tuple<int, int64_t, int64_t, uint64_t>> order;  // insertion order (bounded cache)
-  uint64_t h = 1469598103934665603ull;  // FNV-1a over the z values as used
-  for (int64_t r = 0; r < batch; ++r) {
-    const double* zz = z + (z_stride ? r * z_stride : 0);
-    uint64_t bits[2];
-    std::memcpy(bits, zz, sizeof(bits));
-    for (int w = 0; w < 2; ++w)
-      for (int b = 0; b < 8; ++b) h = (h ^ ((bits[w] >> (8 * b)) & 0xff)) * 1099511628211ull;
-  }
-  const auto key = std::make_tuple(dev, batch, n, h);
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) {
-    *out = &it->second;
+namespace {
+// one Mehler transform with a resolved plan (stream-ordered, capturable)
+int mehler_run(const void* in, void* out, const MehlerPlan& plan, void* workspace, cudaStream_t st) {
+  const int dev = plan.dev;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n = plan.n;
+  int rc = XFT_OK;
+  // per launched CTA one kernel-spectrum row of the largest in-CTA class, then
+  // the four-step classes' spectrum + data rows (2 x count x M)
+  const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << plan.maxl) * sizeof(double2);
+  size_t all_bytes = 0;
+  for (const auto& cl : plan.classes)
+    all_bytes += cl.first <= MAXL_C128 ? hs_bytes : 2 * (size_t)cl.second * ((size_t)1 << cl.first) * 16;
+  OpMehler op;
+  op.rows = plan.rows;
+  op.half = host_half_step(n);
+  op.n = (int)n;
+  if (workspace) {  // caller scratch (xft_mehler_workspace_bytes): the classes one after another
+    op.hscratch = static_cast<double2*>(workspace);
+    size_t off = 0;
+    for (const auto& cl : plan.classes) {
+      const long long cnt = cl.second;
+      rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan.list + off, op, st)
+                                 : run_large_mehler(in, out, cnt, plan.list + off, plan.rows, cl.first, n, st);
+      if (rc) return rc;
+      off += cnt;
+    }
     return XFT_OK;
   }
-  std::vector<OpMehlerRow> rows(batch);
-  std::map<int, std::vector<int>> classes;
-  for (int64_t r = 0; r < batch; ++r) {
-    const double* zz = z + (z_stride ? r * z_stride : 0);
-    const MehlerPlanRow pr = mehler_row(std::complex<double>(zz[0], zz[1]), n);
-    rows[r] = pr.p;
-    classes[pr.l].push_back((int)r);
-  }
-  MehlerPlan p;
-  std::vector<int> list;
-  list.reserve(batch);
-  for (auto& kv : classes) {
-    list.insert(list.end(), kv.second.begin(), kv.second.end());
-    p.classes.emplace_back(kv.first, (long long)kv.second.size());
-    if (kv.first <= MAXL_C128) p.maxl = kv.first;
-  }
-  if (cudaMalloc(&p.rows, batch * sizeof(OpMehlerRow)) != cudaSuccess ||
-      cudaMalloc(&p.list, batch * sizeof(int)) != cudaSuccess ||
-      cudaMemcpy(p.rows, rows.data(), batch * sizeof(OpMehlerRow), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(p.list, list.data(), batch * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
-    cudaFree(p.rows);
-    cudaFree(p.list);
-    return XFT_ECUDA;
-  }
-  if (order.size() >= 8) {  // bounded: drop the oldest plan (callers are stream-ordered behind us)
-    auto old = cache.find(order.front());
-    if (old != cache.end()) {
-      cudaDeviceSynchronize();
-      cudaFree(old->second.rows);
-      cudaFree(old->second.list);
-      cache.erase(old);
+  // Size classes are disjoint row sets: each runs on its own internal stream
+  // (forked from and joined back to `st`, so the call stays stream-ordered and
+  // graph-capturable) with its own scratch, and the small in-CTA classes fill
+  // the SMs the four-step classes' short tile kernels leave idle.
+  char* base = static_cast<char*>(stream_scratch(dev, st, all_bytes));
+  if (!base) return XFT_ECUDA;
+  SideStreams& ss = side_streams(dev, st, (int)plan.classes.size());
+  if (!ss.ok) return XFT_ECUDA;
+  std::lock_guard<std::mutex> lock(ss.mu);
+  if (cudaEventRecord(ss.fork, st) != cudaSuccess) return XFT_ECUDA;
+  size_t forked = 0, off = 0, boff = 0;
+  for (size_t c = 0; c < plan.classes.size() && !rc; ++c) {
+    const auto& cl = plan.classes[c];
+    const long long cnt = cl.second;
+    cudaStream_t sc = ss.st[c];
+    if (cudaStreamWaitEvent(sc, ss.fork, 0) != cudaSuccess) {
+      rc = XFT_ECUDA;
+      break;
     }
-    order.erase(order.begin());
+    forked = c + 1;
+    if (cl.first <= MAXL_C128) {
+      OpMehler oc = op;
+      oc.hscratch = reinterpret_cast<double2*>(base + boff);
+      boff += hs_bytes;
+      rc = blue<double2>(cl.first, in, out, cnt, plan.list + off, oc, sc);
+    } else {
+      rc = run_large_mehler(in, out, cnt, plan.list + off, plan.rows, cl.first, n, sc, base + boff);
+      boff += 2 * (size_t)cnt * ((size_t)1 << cl.first) * 16;
+    }
+    off += cnt;
   }
-  order.push_back(key);
-  *out = &cache.emplace(key, std::move(p)).first->second;
-  return XFT_OK;
+  for (size_t c = 0; c < forked; ++c) {  // join every forked stream (also after an error: `st` stays consistent)
+    if (cudaEventRecord(ss.join[c], ss.st[c]) != cudaSuccess || cudaStreamWaitEvent(st, ss.join[c], 0) != cudaSuccess)
+      rc = rc ? rc : XFT_ECUDA;
+  }
+  return rc;
 }
+}  // namespace
 
 extern "C" {
 
@@ -373,70 +538,72 @@ int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double
   int rc = xft_validate_mehler_z(z, batch, z_stride, nullptr);
   if (rc) return rc;
   if (batch == 0) return XFT_OK;
-  auto st = static_cast<cudaStream_t>(stream);
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const MehlerPlan* plan = nullptr;
-  if ((rc = mehler_plan(dev, batch, n, z, z_stride, &plan))) return rc;
-  // per launched CTA one kernel-spectrum row of the largest in-CTA class, then
-  // the four-step classes' spectrum + data rows (2 x count x M)
-  const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << plan->maxl) * sizeof(double2);
-  size_t large_bytes = 0, all_bytes = 0;
-  for (const auto& cl : plan->classes) {
-    const size_t b = cl.first <= MAXL_C128 ? hs_bytes : 2 * (size_t)cl.second * ((size_t)1 << cl.first) * 16;
-    if (cl.first > MAXL_C128) large_bytes = std::max(large_bytes, b);
-    all_bytes += b;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
+  std::shared_ptr<const MehlerPlan> plan;  // held for the whole call: eviction cannot free it under us
+  if ((rc = cached_mehler_plan(dev, batch, n, z, z_stride, &plan))) return rc;
+  return mehler_run(in, out, *plan, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int xft_mehler_plan_create(int64_t batch, int64_t n, const double* z, int64_t z_stride, void** plan) {
+  if (!plan) return XFT_EPARAM;
+  *plan = nullptr;
+  if (n < 1 || batch < 1) return XFT_EINVALID_SIZE;
+  int rc = xft_validate_mehler_z(z, batch, z_stride, nullptr);
+  if (rc) return rc;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
+  std::shared_ptr<const MehlerPlan> p;
+  if ((rc = build_mehler_plan(dev, batch, n, gather_z(batch, z, z_stride), &p))) return rc;
+  *plan = new std::shared_ptr<const MehlerPlan>(std::move(p));
+  return XFT_OK;
+}
+
+int xft_mehler_plan_destroy(void* plan) {
+  delete static_cast<std::shared_ptr<const MehlerPlan>*>(plan);
+  return XFT_OK;
+}
+
+int xft_mehler_planned(const void* in, void* out, const void* plan, void* workspace, void* stream) {
+  if (!plan) return XFT_EPARAM;
+  const auto& p = *static_cast<const std::shared_ptr<const MehlerPlan>*>(plan);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
+  if (dev != p->dev) return XFT_EPARAM;  // a plan lives on the device it was created on
+  return mehler_run(in, out, *p, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int xft_release_caches(void) {
+  std::vector<std::shared_ptr<const MehlerPlan>> drop;
+  {
+    PlanCache& c = plan_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    drop.swap(c.lru);
+    c.map.clear();
   }
-  OpMehler op;
-  op.rows = plan->rows;
-  op.half = host_half_step(n);
-  op.n = (int)n;
-  if (workspace) {  // caller scratch (xft_mehler_workspace_bytes): the classes one after another
-    op.hscratch = static_cast<double2*>(workspace);
-    size_t off = 0;
-    for (const auto& cl : plan->classes) {
-      const long long cnt = cl.second;
-      rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan->list + off, op, st)
-                                 : run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, st);
-      if (rc) return rc;
-      off += cnt;
-    }
-    return XFT_OK;
+  std::vector<std::pair<int, void*>> bufs;
+  {
+    std::lock_guard<std::mutex> rl(retired().mu);
+    for (auto& p : retired().plans) drop.push_back(std::move(p));
+    retired().plans.clear();
+    bufs.swap(retired().buffers);
   }
-  // Size classes are disjoint row sets: each runs on its own internal stream
-  // (forked from and joined back to `st`, so the call stays stream-ordered and
-  // graph-capturable) with its own scratch, and the small in-CTA classes fill
-  // the SMs the four-step classes' short tile kernels leave idle.
-  char* base = static_cast<char*>(stream_scratch(dev, st, all_bytes));
-  if (!base) return XFT_ECUDA;
-  SideStreams& ss = side_streams(dev, st, (int)plan->classes.size());
-  if (!ss.ok) return XFT_ECUDA;
-  std::lock_guard<std::mutex> lock(ss.mu);
-  if (cudaEventRecord(ss.fork, st) != cudaSuccess) return XFT_ECUDA;
-  size_t off = 0, boff = 0;
-  for (size_t c = 0; c < plan->classes.size() && !rc; ++c) {
-    const auto& cl = plan->classes[c];
-    const long long cnt = cl.second;
-    cudaStream_t sc = ss.st[c];
-    if (cudaStreamWaitEvent(sc, ss.fork, 0) != cudaSuccess) return XFT_ECUDA;
-    if (cl.first <= MAXL_C128) {
-      OpMehler oc = op;
-      oc.hscratch = reinterpret_cast<double2*>(base + boff);
-      boff += hs_bytes;
-      rc = blue<double2>(cl.first, in, out, cnt, plan->list + off, oc, sc);
-    } else {
-      rc = run_large_mehler(in, out, cnt, plan->list + off, plan->rows, cl.first, n, sc, base + boff);
-      boff += 2 * (size_t)cnt * ((size_t)1 << cl.first) * 16;
-    }
-    off += cnt;
+  {
+    ScratchPool& sp = scratch_pool();
+    std::lock_guard<std::mutex> lock(sp.mu);
+    for (auto& kv : sp.pool)
+      if (kv.second.first) bufs.emplace_back(kv.first.first, kv.second.first);
+    sp.pool.clear();
   }
-  for (size_t c = 0; c < plan->classes.size(); ++c) {  // join (also after an error: keep `st` consistent)
-    if (cudaEventRecord(ss.join[c], ss.st[c]) != cudaSuccess || cudaStreamWaitEvent(st, ss.join[c], 0) != cudaSuccess)
-      return XFT_ECUDA;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& b : bufs) {
+    cudaSetDevice(b.first);
+    cudaFree(b.second);
   }
-  (void)large_bytes;
-  return rc;
+  cudaSetDevice(cur);
+  drop.clear();  // plans still held by a caller's handle or an in-flight call survive (refcount)
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
 }
 
 }  // extern "C"

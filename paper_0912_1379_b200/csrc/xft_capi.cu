@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <cstring>
 #include <utility>
@@ -106,7 +107,7 @@ int launch_pipe(const LaunchArgs& a) {
   using SH = PipeShape<C, L>;
   using Cfg = PipeCfg<C, L, SH::E, MODE, SIGN, SH::ROWS, SH::STAGES, SH::MINB, 1>;
   auto kern = xft_pipe_kernel<Cfg>;
-  static int occ_cache[64] = {0};
+  static std::atomic<int> occ_cache[64];  // resident CTAs x SMs per device (0 = not yet queried)
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
@@ -122,13 +123,14 @@ int launch_pipe(const LaunchArgs& a) {
       return XFT_ECUDA;
   }
 #endif
-  int& occ = occ_cache[dev & 63];
-  if (occ == 0) {
+  int occ = occ_cache[dev & 63].load(std::memory_order_relaxed);
+  if (occ == 0) {  // idempotent: concurrent first calls compute and store the same value
     int o = 0, sms = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::THREADS, Cfg::SMEM) != cudaSuccess)
       return XFT_ECUDA;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return XFT_ECUDA;
     occ = (o < 1 ? 1 : o) * sms;
+    occ_cache[dev & 63].store(occ, std::memory_order_relaxed);
   }
   const long long tiles = (a.batch + Cfg::ROWS - 1) / Cfg::ROWS;
   long long cap = occ;
@@ -397,7 +399,7 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
     const int segl = log2_exact(nc);
     rc = run_rows(MODE_LCT, -1, in, workspace, n_rows, n_cols, dtype, nullptr, 0, ur, 0, st, segl, n_rows * nc);
     if (rc) return rc;
-    // the 8 slabs are independent: two internal streams (forked from / joined to
+    // the 8 slabs are independent: internal streams (forked from / joined to
     // `st`) so one slab's column kernel starts on the SMs another's tail frees
     int dev = 0;
     cudaGetDevice(&dev);
@@ -405,23 +407,31 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
     if (!ss.ok) return XFT_ECUDA;
     std::lock_guard<std::mutex> lock(ss.mu);
     if (cudaEventRecord(ss.fork, st) != cudaSuccess) return XFT_ECUDA;
-    for (int q = 0; q < XFT_LCT2D_LANES; ++q)
-      if (cudaStreamWaitEvent(ss.st[q], ss.fork, 0) != cudaSuccess) return XFT_ECUDA;
+    int forked = 0;
+    for (; forked < XFT_LCT2D_LANES; ++forked)
+      if (cudaStreamWaitEvent(ss.st[forked], ss.fork, 0) != cudaSuccess) {
+        rc = XFT_ECUDA;
+        break;
+      }
     for (int h = 0; h < 8 && !rc; ++h) {
       cudaStream_t sh = ss.st[h % XFT_LCT2D_LANES];
       const char* slab = static_cast<const char*>(workspace) + esz * (size_t)h * n_rows * nc;
       char* dst = static_cast<char*>(out) + esz * (size_t)h * nc;
       rc = run_lct_cols_cluster(slab, dst, n_rows, nc, nc, n_cols, dtype, abcd_col, 0, sh);
-      if (rc == XFT_ENOTSUP) {  // no cluster path here: columns in place on the slab, then place it
-        rc = run_lct_cols(slab, const_cast<char*>(slab), nullptr, n_rows, nc, nc, dtype, abcd_col, 0, sh);
+      if (rc == XFT_ENOTSUP) {
+        // no cluster path on this device/shape (e.g. MIG/MPS, no 16-CTA clusters): the
+        // two-pass column transform on the slab with its own [n_rows][nc] scratch (per
+        // lane stream), then place the slab's columns into `out`
+        void* cs = stream_scratch(dev, sh, esz * (size_t)n_rows * nc);
+        rc = cs ? run_lct_cols(slab, const_cast<char*>(slab), cs, n_rows, nc, nc, dtype, abcd_col, 0, sh) : XFT_ECUDA;
         if (!rc && cudaMemcpy2DAsync(dst, esz * n_cols, slab, esz * nc, esz * nc, n_rows, cudaMemcpyDeviceToDevice,
                                      sh) != cudaSuccess)
           rc = XFT_ECUDA;
       }
     }
-    for (int q = 0; q < XFT_LCT2D_LANES; ++q)
+    for (int q = 0; q < forked; ++q)  // join every forked lane, also after an error (`st` stays consistent)
       if (cudaEventRecord(ss.join[q], ss.st[q]) != cudaSuccess || cudaStreamWaitEvent(st, ss.join[q], 0) != cudaSuccess)
-        return XFT_ECUDA;
+        rc = rc ? rc : XFT_ECUDA;
     return rc;
   }
   // axis 1: rows (in -> out); axis 0: columns in place on `out` (workspace = four-step scratch)

@@ -22,6 +22,11 @@ struct SideStreams {
 };
 SideStreams& side_streams(int dev, cudaStream_t caller, int count);
 
+// per-(device, stream) scratch of at least `bytes`, grown on demand; superseded
+// buffers are retired (kept alive until xft_release_caches), never freed under
+// queued work; legal during stream capture.  nullptr on allocation failure.
+void* stream_scratch(int dev, cudaStream_t st, size_t bytes);
+
 // chirp-z route for lengths that are not powers of two (xft_bluestein.cu);
 // mode: 0 DFT (sign), 1 scaled Fourier, 2 LCT.  abcd: device, stride 0|4.
 int run_chirpz(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,

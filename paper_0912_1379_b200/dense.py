@@ -55,8 +55,7 @@ def dense_lct_apply(values, abcd=None, *, out=None):
         p = np.ascontiguousarray(np.asarray(abcd, dtype=np.float64).reshape(4))
         if p[1] == 0:
             raise DegenerateParameterError("b = 0 has no kernel matrix; use lct_b_zero")
-    if out is None:
-        out = torch.empty_like(v)
+    out = ops.check_out(out, v)
     with torch.cuda.device(v.device):
         _native.call("xft_dense_lct_apply", v.data_ptr(), out.data_ptr(), B, n,
                      None if p is None else p.ctypes.data, ops._stream_ptr(v.device))
@@ -74,8 +73,7 @@ def dense_mehler_apply(values, z, *, out=None):
     if zz.shape[0] not in (1, B):
         raise ShapeError(f"{zz.shape[0]} orders for a batch of {B}")
     zh = np.ascontiguousarray(np.stack([zz.real, zz.imag], axis=1))
-    if out is None:
-        out = torch.empty_like(v)
+    out = ops.check_out(out, v)
     with torch.cuda.device(v.device):
         _native.call("xft_dense_mehler_apply", v.data_ptr(), out.data_ptr(), B, n, zh.ctypes.data,
                      0 if zh.shape[0] == 1 else 2, ops._stream_ptr(v.device))

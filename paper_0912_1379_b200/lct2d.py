@@ -33,13 +33,11 @@ def lct2d(field, abcd_row, abcd_col=None, *, out=None, workspace=None):
         abcd_col = abcd_row
     if field.dim() != 2 or not field.is_cuda:
         raise ShapeError("lct2d needs a 2-D CUDA tensor")
-    f = field.contiguous()
+    f = ops.aligned(field)
     r, c = f.shape
     pr, pc = _abcd4(abcd_row), _abcd4(abcd_col)
-    if out is None:
-        out = torch.empty_like(f)
-    if workspace is None:
-        workspace = torch.empty_like(f)
+    out = ops.check_out(out, f)
+    workspace = ops.check_out(workspace, f)
     with torch.cuda.device(f.device):
         _native.call("xft_lct2d", f.data_ptr(), out.data_ptr(), r, c, ops._dtype_code(f),
                      pr.ctypes.data, pc.ctypes.data, workspace.data_ptr(), ops._stream_ptr(f.device))
@@ -54,8 +52,8 @@ def rows_packed(local, abcd_row, world: int, out=None):
     nc = n // world
     if nc * world != n or nc & (nc - 1):
         raise ShapeError(f"n = {n} must split into {world} power-of-two column blocks")
-    if out is None:
-        out = torch.empty((world, rl, nc), dtype=local.dtype, device=local.device)
+    local = ops.aligned(local)
+    out = ops.check_out(out, local, (world, rl, nc))
     p = _abcd4(abcd_row)
     with torch.cuda.device(local.device):
         _native.call("xft_lct_rows_packed", local.data_ptr(), out.data_ptr(), rl, n, ops._dtype_code(local),
@@ -87,9 +85,11 @@ def columns_inplace(slab, abcd_col, workspace=None):
     """Column LCT of a row-major [n, nc] slab, in place."""
     torch = ops._torch()
     n, nc = slab.shape
+    if not slab.is_contiguous() or slab.data_ptr() % ops.ALIGN:
+        raise ShapeError("the column slab is transformed in place: it must be contiguous and 16-byte aligned")
     p = _abcd4(abcd_col)
-    if workspace is None and n > 1024:
-        workspace = torch.empty_like(slab)
+    if n > 1024:
+        workspace = ops.check_out(workspace, slab)
     with torch.cuda.device(slab.device):
         _native.call("xft_lct_columns", slab.data_ptr(), slab.data_ptr(), n, nc, nc, ops._dtype_code(slab),
                      p.ctypes.data, 0 if workspace is None else workspace.data_ptr(), ops._stream_ptr(slab.device))

@@ -72,12 +72,73 @@ def mehler_rows(values, z, *, out=None):
     if zz.shape[0] not in (1, B):
         raise ShapeError(f"{zz.shape[0]} orders for a batch of {B}")
     zh = np.ascontiguousarray(np.stack([zz.real, zz.imag], axis=1))
-    if out is None:
-        out = torch.empty_like(v)
+    out = ops.check_out(out, v)
     with torch.cuda.device(v.device):
         _native.call("xft_mehler", v.data_ptr(), out.data_ptr(), B, n, zh.ctypes.data,
                      0 if zh.shape[0] == 1 else 2, None, ops._stream_ptr(v.device))
     return out
+
+
+class MehlerPlan:
+    """Caller-owned device plan for one z array (``xft_mehler_plan_create``).
+
+    The per-row parameters, size classes and row lists that ``mehler_rows``
+    otherwise takes from the library's implicit cache, held by the caller: a
+    CUDA graph captured around ``apply`` stays valid for as long as the plan
+    object lives, whatever else the process transforms.  Immutable; ``apply``
+    may run from several threads/streams at once.  ``close()`` (or garbage
+    collection) frees it -- only after the work and graphs using it are done.
+    """
+
+    def __init__(self, n: int, z, device=None):
+        import ctypes
+
+        torch = ops._torch()
+        zz = _check_z(z)
+        self.n, self.batch = int(n), int(zz.shape[0])
+        if self.n < 1:
+            raise InvalidSizeError(f"transform length must be positive, got {n!r}")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        zh = np.ascontiguousarray(np.stack([zz.real, zz.imag], axis=1))
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.call("xft_mehler_plan_create", self.batch, self.n, zh.ctypes.data, 2, ctypes.byref(h))
+        self._h = h.value
+
+    def apply(self, values, *, out=None):
+        torch = ops._torch()
+        if self._h is None:
+            raise ParameterError("the plan has been closed")
+        v = ops._rows_view(values)
+        if v.dtype != torch.complex128:
+            raise ParameterError("the Mehler transform runs in complex128 (1e-12 tolerance)")
+        if tuple(v.shape) != (self.batch, self.n):
+            raise ShapeError(f"plan is for [{self.batch}, {self.n}], got {tuple(v.shape)}")
+        if v.device != self.device:
+            raise ShapeError(f"plan lives on {self.device}, values on {v.device}")
+        out = ops.check_out(out, v)
+        with torch.cuda.device(v.device):
+            _native.call("xft_mehler_planned", v.data_ptr(), out.data_ptr(), self._h, None,
+                         ops._stream_ptr(v.device))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            _native.lib().xft_mehler_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def release_caches():
+    """Frees the implicit plan cache, retired plans and internal scratch (``xft_release_caches``).
+
+    Call only when no queued work or live CUDA graph uses them."""
+    _native.call("xft_release_caches")
 
 
 @dataclass(frozen=True)

@@ -35,6 +35,17 @@ def _stream_ptr(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+ALIGN = 16  # bytes: rows move with cp.async.bulk (include/xft_b200.h "Alignment")
+
+
+def aligned(t):
+    """``t`` contiguous and 16-byte aligned (a copy when the view is not)."""
+    t = t.contiguous()
+    if t.numel() and t.data_ptr() % ALIGN:
+        t = t.clone()  # fresh allocations are 256-byte aligned
+    return t
+
+
 def _rows_view(values, what="values"):
     if values.dim() == 1:
         values = values.unsqueeze(0)
@@ -44,7 +55,46 @@ def _rows_view(values, what="values"):
         raise InvalidSizeError(f"transform length must be positive, got {values.shape[1]}")
     if not values.is_cuda:
         raise ShapeError(f"{what} must be a CUDA tensor")
-    return values.contiguous()
+    return aligned(values)
+
+
+def check_out(out, like, shape=None):
+    """A caller-supplied ``out`` must match exactly: shape, dtype, device, contiguous, 16-byte aligned.
+
+    (The kernels write through the raw pointer; a wrong ``out`` would be an
+    out-of-bounds device write.)  Returns ``out``; allocates when it is None."""
+    torch = _torch()
+    shape = tuple(like.shape) if shape is None else tuple(shape)
+    if out is None:
+        return torch.empty(shape, dtype=like.dtype, device=like.device)
+    if not isinstance(out, torch.Tensor):
+        raise ShapeError(f"out must be a torch tensor, got {type(out).__name__}")
+    if tuple(out.shape) != shape:
+        raise ShapeError(f"out has shape {tuple(out.shape)}, expected {shape}")
+    if out.dtype != like.dtype:
+        raise ParameterError(f"out has dtype {out.dtype}, expected {like.dtype}")
+    if out.device != like.device:
+        raise ShapeError(f"out is on {out.device}, expected {like.device}")
+    if not out.is_contiguous():
+        raise ShapeError("out must be contiguous")
+    if out.numel() and out.data_ptr() % ALIGN:
+        raise ShapeError(f"out must be {ALIGN}-byte aligned")
+    return out
+
+
+def check_out_host(out, like: np.ndarray):
+    """Host-buffer variant of ``check_out`` for numpy arrays."""
+    if out is None:
+        return np.empty_like(like)
+    if not isinstance(out, np.ndarray):
+        raise ShapeError(f"out must be a numpy array, got {type(out).__name__}")
+    if out.shape != like.shape:
+        raise ShapeError(f"out has shape {out.shape}, expected {like.shape}")
+    if out.dtype != like.dtype:
+        raise ParameterError(f"out has dtype {out.dtype}, expected {like.dtype}")
+    if not out.flags.c_contiguous or not out.flags.writeable:
+        raise ShapeError("out must be a writeable C-contiguous array")
+    return out
 
 
 def validate_abcd_host(abcd: np.ndarray, check_unimodular=True, tol=UNIMODULAR_TOL) -> None:
@@ -83,8 +133,7 @@ def lct_rows(values, abcd, *, bare_fourier=False, out=None, validate=True,
     if p_dev.shape[0] not in (1, B):
         raise ShapeError(f"abcd has {p_dev.shape[0]} rows for a batch of {B}")
     stride = 0 if p_dev.shape[0] == 1 else 4
-    if out is None:
-        out = torch.empty_like(v)
+    out = check_out(out, v)
     flags = _native.FLAG_BARE_FOURIER if bare_fourier else 0
     with torch.cuda.device(v.device):
         _native.call("xft_lct", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v),
@@ -101,8 +150,7 @@ def dft_rows(values, sign: int, *, out=None):
         raise ParameterError(f"direction_sign must be +1 or -1, got {sign!r}")
     v = _rows_view(values)
     B, n = v.shape
-    if out is None:
-        out = torch.empty_like(v)
+    out = check_out(out, v)
     with torch.cuda.device(v.device):
         _native.call("xft_dft", v.data_ptr(), out.data_ptr(), B, n, int(sign), _dtype_code(v),
                      _stream_ptr(v.device))
@@ -114,8 +162,7 @@ def scaled_fourier_rows(values, *, out=None):
     torch = _torch()
     v = _rows_view(values)
     B, n = v.shape
-    if out is None:
-        out = torch.empty_like(v)
+    out = check_out(out, v)
     with torch.cuda.device(v.device):
         _native.call("xft_scaled_fourier", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v),
                      _stream_ptr(v.device))
@@ -127,10 +174,9 @@ def transpose(values, *, out=None):
     torch = _torch()
     if values.dim() != 2 or not values.is_cuda:
         raise ShapeError("transpose needs a 2-D CUDA tensor")
-    v = values.contiguous()
+    v = aligned(values)
     r, c = v.shape
-    if out is None:
-        out = torch.empty((c, r), dtype=v.dtype, device=v.device)
+    out = check_out(out, v, (c, r))
     with torch.cuda.device(v.device):
         _native.call("xft_transpose", v.data_ptr(), out.data_ptr(), r, c, c, r, _dtype_code(v),
                      _stream_ptr(v.device))
@@ -157,12 +203,16 @@ def lct_host(values: np.ndarray, abcd, *, bare_fourier=False, out=None,
     p = np.ascontiguousarray(np.asarray(abcd, dtype=np.float64).reshape(-1, 4))
     if p.shape[0] not in (1, v.shape[0]):
         raise ShapeError(f"abcd has {p.shape[0]} rows for a batch of {v.shape[0]}")
-    if out is None:
-        out = np.empty_like(v)
+    if v.ctypes.data % ALIGN:
+        v = v.copy()  # numpy allocations are 16-byte aligned; a misaligned view is copied
+    res = check_out_host(None if out is None else (out[None, :] if out.ndim == 1 else out), v)
+    dst = res if res.ctypes.data % ALIGN == 0 else np.empty_like(v)
     flags = _native.FLAG_BARE_FOURIER if bare_fourier else 0
-    _native.call("xft_lct_host", v.ctypes.data, out.ctypes.data, v.shape[0], v.shape[1], code,
+    _native.call("xft_lct_host", v.ctypes.data, dst.ctypes.data, v.shape[0], v.shape[1], code,
                  p.ctypes.data, 0 if p.shape[0] == 1 else 4, flags, int(bool(check_unimodular)), float(tol))
-    return out
+    if dst is not res:
+        res[...] = dst
+    return res if out is None or out.ndim != 1 else out
 
 
 def lct_chain_rows(values, stages, *, scale=1.0, reverse=False, out=None):
@@ -175,8 +225,7 @@ def lct_chain_rows(values, stages, *, scale=1.0, reverse=False, out=None):
     v = _rows_view(values)
     B, n = v.shape
     p = np.ascontiguousarray(np.asarray(stages, dtype=np.float64).reshape(-1, 4))
-    if out is None:
-        out = torch.empty_like(v)
+    out = check_out(out, v)
     if B == 0:
         return out
     if not 1 <= p.shape[0] <= 4:
@@ -228,8 +277,7 @@ def lct_b_zero_rows(samples, abcd, *, out=None, tol=UNIMODULAR_TOL):
         from .errors import raise_for
         raise_for(st, f"b = 0 parameters (row {bad.value})")
     p_dev = torch.from_numpy(p_host).to(v.device)
-    if out is None:
-        out = torch.empty_like(v)
+    out = check_out(out, v)
     with torch.cuda.device(v.device):
         _native.call("xft_lct_b_zero", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v), p_dev.data_ptr(),
                      0 if p_host.shape[0] == 1 else 4, _stream_ptr(v.device))

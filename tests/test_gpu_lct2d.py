@@ -175,3 +175,33 @@ def test_sharded_p2p_symmetric_memory_world1(torch, L2, tmp_path):
         assert rel_l2(got.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.slow
+def test_slab_route_without_cluster_kernel(torch):
+    """The single-GPU 2-D slab route on a build without the cluster column kernel (XFT_COLCLU=0,
+    the path MIG/MPS devices take when no 16-CTA cluster fits) gives the default build's result."""
+    import os
+    import subprocess
+
+    from paper_0912_1379_b200 import _native, lct2d
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    so = os.path.join(root, "tune", "libxft_noclu.so")
+    if not os.path.exists(so):
+        subprocess.run(["bash", os.path.join(root, "tools", "build_variant.sh"), "noclu", "-DXFT_COLCLU=0"],
+                       check=True, timeout=900)
+    rng = np.random.default_rng(21)
+    n = 2048
+    f = torch.from_numpy((rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(np.complex64)).cuda()
+    p = (1.0, 0.25, 0.0, 1.0)
+    ref = lct2d.lct2d(f, p, p)
+    saved = _native.lib()
+    try:
+        _native._lib = _native.load_library(so)
+        got = lct2d.lct2d(f, p, p)
+        torch.cuda.synchronize()
+    finally:
+        _native._lib = saved
+    err = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
+    assert err <= 2e-6, err

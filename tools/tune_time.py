@@ -12,6 +12,10 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _variant import use_variant  # noqa: E402
+
+use_variant()
 
 
 def main():
