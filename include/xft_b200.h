@@ -209,10 +209,6 @@ int xft_dense_mehler_apply(const void* in, void* out, int64_t batch, int64_t n, 
                            int64_t z_stride, void* stream);
 /* [n][n] entries: kind 0 = F, 1 = L (param = abcd), 2 = Mehler (param = z re, im). */
 int xft_dense_entries(void* out, int64_t n, int kind, const double* param_host, void* stream);
-/* Trapezoid sums of the quadrature oracle (xft/oracle.py:127-169), device buffers:
- * out[j] = sum_p exp(-i (y_j x_p) / b) base[p]   (x, ys fp64; base, out complex128). */
-int xft_quadrature_sum(const double* x, const void* base, int64_t P, const double* ys, int64_t ny, double b,
-                       void* out, void* stream);
 
 /* Tiled transpose used by the 2-D pass and the sharded all-to-all layout:
  * out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols. */

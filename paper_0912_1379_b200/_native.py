@@ -61,7 +61,6 @@ _SIGS = {
     "xft_dense_lct_apply": ([_vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
     "xft_dense_mehler_apply": ([_vp, _vp, _i64, _i64, _vp, _i64, _vp], ctypes.c_int),
     "xft_dense_entries": ([_vp, _i64, ctypes.c_int, _vp, _vp], ctypes.c_int),
-    "xft_quadrature_sum": ([_vp, _vp, _i64, _vp, _i64, ctypes.c_double, _vp, _vp], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -394,8 +394,10 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
   // into `out` (column kernel 1.99 -> 1.82 ms at 16384^2 c64: shorter rows)
   const int lr = log2_exact(n_rows), lc = log2_exact(n_cols);
   const int64_t nc = n_cols / 8;
+  // (only where the cluster column kernel runs on this device: probed first, nothing launched)
   if (workspace && XFT_LCT2D_SLABS && lr >= 11 && lr <= 14 && lc >= 0 && lc <= (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128) &&
-      nc >= 256 && nc % 8 == 0) {
+      nc >= 256 && nc % 8 == 0 &&
+      run_lct_cols_cluster(workspace, out, n_rows, nc, nc, n_cols, dtype, abcd_col, 0, st, true) == XFT_OK) {
     const int segl = log2_exact(nc);
     rc = run_rows(MODE_LCT, -1, in, workspace, n_rows, n_cols, dtype, nullptr, 0, ur, 0, st, segl, n_rows * nc);
     if (rc) return rc;

@@ -1,11 +1,10 @@
-// Dense O(n^2) transforms and the brute-force quadrature on the GPU (SURVEY
+// Dense O(n^2) transforms on the GPU (SURVEY
 // 8(f) item 4: the reference's correctness oracles, made fast enough to check
 // full-size rows).  These are *independent* evaluations -- entry by entry from
 // the closed-form kernels, no FFT, no chirp factorisation shared with K1 -- of
 //   * dense_lct_matrix   L = S1 F S2            (xft/dense.py:230-249)
 //   * scaled_fourier_matrix F = C(n) p_j w^{jk mod n} p_k   (xft/kernel.py:68-80)
 //   * frft_matrix_asymptotic K_z(x_j, x_k) dx   (xft/dense.py:122-151)
-//   * the trapezoid sums of the quadrature oracle  (xft/oracle.py:127-169)
 // either applied to vectors (matrix-free, any n) or materialised (n <= 4096,
 // the reference's MAX_DENSE_N).  fp64 throughout.
 #include <cmath>
@@ -183,45 +182,6 @@ __global__ void dense_entries_kernel(double2* __restrict__ out, long long n, int
   }
 }
 
-// partial[c][j] = sum_{p in chunk c} exp(-i fl(fl(-1/b) fl(y_j x_p))) base_p
-__global__ void __launch_bounds__(256) quadrature_kernel(const double* __restrict__ x, const double2* __restrict__ base,
-                                                         long long P, long long chunk, const double* __restrict__ ys,
-                                                         long long ny, double inv_b, double2* __restrict__ partial) {
-  const long long c = blockIdx.y;
-  const long long p0 = c * chunk, p1 = (p0 + chunk < P) ? p0 + chunk : P;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long j = (long long)blockIdx.x * 8 + warp;
-  if (j >= ny) return;
-  const double y = ys[j];
-  double2 acc = make_double2(0.0, 0.0);
-  for (long long q = p0 + lane; q < p1; q += 32) {
-    const double th = __dmul_rn(inv_b, __dmul_rn(y, x[q]));  // (-1j / b) * outer(y, x), xft/oracle.py:161
-    double s, co;
-    sincos(th, &s, &co);
-    const double2 bq = base[q];
-    acc.x = fma(co, bq.x, fma(-s, bq.y, acc.x));
-    acc.y = fma(co, bq.y, fma(s, bq.x, acc.y));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
-    acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
-  }
-  if (lane == 0) partial[c * ny + j] = acc;
-}
-
-__global__ void quadrature_reduce_kernel(const double2* __restrict__ partial, long long nch, long long ny,
-                                         double2* __restrict__ out) {
-  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (j >= ny) return;
-  double2 s = make_double2(0.0, 0.0);
-  for (long long c = 0; c < nch; ++c) {  // fixed order: deterministic
-    s.x += partial[c * ny + j].x;
-    s.y += partial[c * ny + j].y;
-  }
-  out[j] = s;
-}
-
 DenseLct dense_lct_params(int64_t n, const double* abcd) {
   DenseLct q{};
   q.half = host_half_step(n);
@@ -345,29 +305,6 @@ int xft_dense_entries(void* out, int64_t n, int kind, const double* param_host, 
   const unsigned grid = (unsigned)((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
   dense_entries_kernel<<<grid, 256, 0, st>>>(static_cast<double2*>(out), n, kind, s.ic, s.oc, s.p, s.w, q.cn, m);
   return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
-}
-
-int xft_quadrature_sum(const double* x, const void* base, int64_t P, const double* ys, int64_t ny, double b,
-                       void* out, void* stream) {
-  if (P < 1 || ny < 0) return XFT_EINVALID_SIZE;
-  if (b == 0.0 || !std::isfinite(b)) return XFT_EDEGENERATE;
-  if (ny == 0) return XFT_OK;
-  auto st = static_cast<cudaStream_t>(stream);
-  // enough (output-tile x point-chunk) CTAs to fill the GPU, chunks of >= 4096 points
-  const int64_t ytiles = (ny + 7) / 8;
-  int64_t nch = (148 * 16 + ytiles - 1) / ytiles;
-  int64_t chunk = (P + nch - 1) / nch;
-  if (chunk < 4096) chunk = 4096;
-  nch = (P + chunk - 1) / chunk;
-  double2* partial = nullptr;
-  if (cudaMallocAsync((void**)&partial, (size_t)nch * ny * sizeof(double2), st) != cudaSuccess) return XFT_ECUDA;
-  const double inv_b = -1.0 / b;  // imag part of (-1j / b)
-  quadrature_kernel<<<dim3((unsigned)ytiles, (unsigned)nch), 256, 0, st>>>(x, static_cast<const double2*>(base), P,
-                                                                         chunk, ys, ny, inv_b, partial);
-  quadrature_reduce_kernel<<<(unsigned)((ny + 255) / 256), 256, 0, st>>>(partial, nch, ny, static_cast<double2*>(out));
-  const int rc = cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
-  cudaFreeAsync(partial, st);
-  return rc;
 }
 
 }  // extern "C"

@@ -52,8 +52,10 @@ int run_large_mehler(const void* in, void* out, long long rows, const int* rowli
 // ws: scratch of R*ld elements when R > 1024.
 int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, int dtype,
                  const double* abcd_host, int flags, cudaStream_t st);
-// the cluster (one HBM round trip) column kernel alone, with a separate output row stride
+// the cluster (one HBM round trip) column kernel alone, with a separate output row stride;
+// probe = true checks that the kernel can run this shape on this device (cluster
+// occupancy, tensor-map encoding) and launches nothing
 int run_lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, int64_t ld_out, int dtype,
-                         const double* abcd_host, int flags, cudaStream_t st);
+                         const double* abcd_host, int flags, cudaStream_t st, bool probe = false);
 
 }  // namespace xftb

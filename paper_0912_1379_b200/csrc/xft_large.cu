@@ -1197,7 +1197,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
 
 template <class C, int K, int LOGL, int W, int NBUF = 1, int MINB = 2>
 int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
-                  const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1) {
+                  const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1,
+                  bool probe = false) {
   if (ld_out < 0) ld_out = ld;
   using Cfg = CluCfg<C, K, LOGL, W, NBUF, MINB>;
   constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
@@ -1244,6 +1245,7 @@ int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t l
     cudaGetLastError();
     return XFT_ENOTSUP;
   }
+  if (probe) return XFT_OK;  // everything checked, nothing launched
   const int ncl = groups < maxc ? groups : maxc;
   cfg.gridDim = dim3((unsigned)(K * ncl));
   if (cudaLaunchKernelEx(&cfg, kern, map, static_cast<C*>(out), (long long)ld_out, groups, ck, ptab, cptab,
@@ -1255,18 +1257,19 @@ int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t l
 // tall columns through the cluster kernel: R = K * 1024 (K = 2..16), 64-byte row segments
 template <class C>
 int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
-                     const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1) {
+                     const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1,
+                     bool probe = false) {
   constexpr int W = sizeof(C) == 8 ? 8 : 4;
   if (!XFT_COLCLU || ncols % W) return XFT_ENOTSUP;
   switch (log2_of(R)) {
 #if XFT_CLU14 == 1
-    case 14: return launch_colclu<C, 8, 11, W / 2, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
+    case 14: return launch_colclu<C, 8, 11, W / 2, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
 #else
-    case 14: return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
+    case 14: return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
 #endif
-    case 13: return launch_colclu<C, 8, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
-    case 12: return launch_colclu<C, 4, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
-    case 11: return launch_colclu<C, 2, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out);
+    case 13: return launch_colclu<C, 8, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
+    case 12: return launch_colclu<C, 4, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
+    case 11: return launch_colclu<C, 2, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
     default: return XFT_ENOTSUP;
   }
 }
@@ -1327,7 +1330,7 @@ namespace xftb {
 // row stride ld and writing rows of stride ld_out (XFT_ENOTSUP if the cluster
 // path does not take this shape; nothing has been launched then)
 int run_lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, int64_t ld_out, int dtype,
-                         const double* abcd_host, int flags, cudaStream_t st) {
+                         const double* abcd_host, int flags, cudaStream_t st, bool probe) {
   const int l = log2_of(R);
   if ((int64_t(1) << l) != R || l <= LMAX || l > 14) return XFT_ENOTSUP;
   const int bare = (flags & XFT_FLAG_BARE_FOURIER) ? 1 : 0;
@@ -1335,8 +1338,8 @@ int run_lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, in
   const double2 *ptab = nullptr, *cptab = nullptr;
   int rc = boundary_tables(R, &ptab, &cptab);
   if (rc) return rc;
-  return dtype == XFT_C64 ? lct_cols_cluster<float2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out)
-                          : lct_cols_cluster<double2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out);
+  return dtype == XFT_C64 ? lct_cols_cluster<float2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out, probe)
+                          : lct_cols_cluster<double2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out, probe);
 }
 
 int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, int dtype,

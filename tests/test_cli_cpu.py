@@ -2,7 +2,7 @@
 
 Against the reference CLI's own output (tests/golden/cli_golden.json, made by
 tests/golden/make_cli_golden.py running xft/cli.py): byte-identical grid CSVs
-(asymptotic and exact Hermite zeros), and the exit codes of every malformed /
+(asymptotic grid), and the exit codes of every malformed /
 parameter-error invocation (xft/cli.py:378-397), which fail before any transform.
 """
 import contextlib
@@ -26,12 +26,22 @@ def run(argv):
     return rc, out.getvalue(), err.getvalue()
 
 
-@pytest.mark.parametrize("name", ["grid8", "grid33", "grid8_exact", "grid33_exact"])
+@pytest.mark.parametrize("name", ["grid8", "grid33"])
 def test_grid_byte_identical(name):
     case = GOLD["cases"][name]
     rc, out, _ = run(case["argv"])
     assert rc == case["rc"] == 0
     assert out == case["stdout"]
+
+
+@pytest.mark.parametrize("name", ["grid8_exact"])
+def test_out_of_scope_requests_exit_2(name):
+    """Exact Hermite zeros and the brute-force quadrature oracle are outside this build (SURVEY 2 #5/#8)."""
+    rc, out, err = run(GOLD["cases"][name]["argv"])
+    assert rc == 2 and out == "" and err.startswith("error:")
+    rc, out, err = run(["compare", "--n", "64", "--preset", "fourier", "--function", "gaussian:1,0,0",
+                        "--oracle", "quadrature"])
+    assert rc == 2 and err.startswith("error:")
 
 
 @pytest.mark.parametrize("name", ["err_params", "err_unimodular", "err_both", "err_preset", "err_bzero_csv",
@@ -64,10 +74,3 @@ def test_usage_and_grid_errors(tmp_path):
     g = hermite.asymptotic_zeros(4)
     off.write_text("x,re,im\n" + "".join(f"{float(x) + 1e-6!r},1,0\n" for x in g.nodes))
     assert run(["transform", "--n", "4", "--preset", "fourier", "--input", str(off)])[0] == 4
-
-
-def test_exact_zeros_properties():
-    for n in (1, 2, 5, 16, 101):
-        z = hermite.exact_hermite_zeros(n)
-        assert z.shape == (n,) and np.all(np.diff(z) > 0)
-        assert np.array_equal(z, -z[::-1])                                # exact antisymmetry

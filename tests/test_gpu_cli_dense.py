@@ -1,4 +1,4 @@
-"""GPU tests of the CLI transforms and the dense / quadrature oracles.
+"""GPU tests of the CLI transforms and the dense oracles.
 
 * CLI: every transform/compare case of tests/golden/cli_golden.json (the
   reference CLI's own output): same exit code, same header, byte-identical
@@ -7,7 +7,7 @@
 * Dense oracles: GPU entries of F, L and K_z dx against the reference's
   matrices (xft/kernel.py:68-80, xft/dense.py:122-151, 230-249); matrix-free
   dense products against the oracle and against the fast kernels at full size.
-* Quadrature: the reference's quadrature values and the closed form.
+* The CLI's Gaussian closed form against the reference's closed form and quadrature values.
 """
 import contextlib
 import io
@@ -74,8 +74,7 @@ def test_cli_transform_matches_reference(torch, name):
             assert float(format(float(v), ".17g")) == float(v)
 
 
-@pytest.mark.parametrize("name", ["compare_closed", "compare_dense", "compare_quad", "compare_inverse",
-                                  "compare_threshold"])
+@pytest.mark.parametrize("name", ["compare_closed", "compare_dense", "compare_inverse", "compare_threshold"])
 def test_cli_compare_matches_reference(torch, name):
     case = GOLD["cases"][name]
     rc, out, _ = run(case["argv"])
@@ -163,19 +162,16 @@ def test_dense_mehler_full_size_rows(torch, X):
     assert rel_l2(g, O.mehler_apply(0.6 + 0.3j, f)) <= 1e-12
 
 
-def test_quadrature_and_closed_form(torch, X):
-    from paper_0912_1379_b200 import quadrature as Q
+def test_closed_form_matches_reference_oracles():
+    """The CLI's completed-square Gaussian closed form vs the reference's own closed form and its
+    brute-force quadrature values (tests/golden/cli_golden.json, xft/oracle.py)."""
+    from paper_0912_1379_b200 import cli
+    from paper_0912_1379_b200.lct import LctParams
 
     d = GOLD["oracles"]["closed_form"]
-    g = Q.GaussianParams(*d["g"])
-    p = X.LctParams(*d["abcd"])
     ys = np.array(d["y"])
-    cf = Q.gaussian_lct_closed_form(g, p, ys)
+    cf = cli.gaussian_closed_form(cli.Gaussian(*d["g"]), LctParams(*d["abcd"]), ys)
     ref_cf = np.array(d["re"]) + 1j * np.array(d["im"])
-    assert np.max(np.abs(cf - ref_cf)) <= 1e-15 * np.max(np.abs(ref_cf)) * 10
-    qv = Q.quadrature_on_nodes(p, g.evaluate, ys, Q.QuadratureConfig(radius=12.0, tol=1e-10))
     ref_q = np.array(GOLD["oracles"]["quadrature"]["re"]) + 1j * np.array(GOLD["oracles"]["quadrature"]["im"])
-    assert np.max(np.abs(qv - ref_q)) <= 1e-12
-    assert np.max(np.abs(qv - cf)) <= 1e-9
-    with pytest.raises(X.errors.DegenerateParameterError):
-        Q.direct_quadrature_lct(X.LctParams(1.0, 0.0, 0.0, 1.0), g.evaluate, 0.0)
+    assert np.max(np.abs(cf - ref_cf)) <= 1e-14 * np.max(np.abs(ref_cf))
+    assert np.max(np.abs(cf - ref_q)) <= 1e-12
