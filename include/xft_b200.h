@@ -101,6 +101,15 @@ int xft_validate_lct_params(const double* abcd, int64_t count, int64_t stride, i
 int xft_lct(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
             int64_t abcd_stride, int flags, void* stream);
 
+/* xft_lct plus the reference's finite-input check (Signal, xft/lct.py:125-126) fused
+ * into the row kernel's loads (no extra HBM pass on the pipelined path; the short-row,
+ * chirp-z and four-step paths scan first): *bad_row (DEVICE int64) receives the
+ * smallest row index holding an Inf/NaN sample, or INT64_MAX if every row is finite.
+ * Stream-ordered: read it after the stream has reached this point.  The transform
+ * itself runs either way (rows with non-finite input give non-finite output). */
+int xft_lct_checked(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+                    int64_t abcd_stride, int flags, int64_t* bad_row, void* stream);
+
 /* Batched unnormalised DFT, sign = +1 or -1 (device pointers).
  * Replaces apply_dft(plan_dft(n, sign), v) (xft/fftcore.py:103-119). */
 int xft_dft(const void* in, void* out, int64_t batch, int64_t n, int sign, int dtype, void* stream);
@@ -158,6 +167,20 @@ int xft_release_caches(void);
 int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dtype, const double* abcd_row,
               const double* abcd_col, void* workspace, void* stream);
 
+/* Sharded separable 2-D LCT over NCCL: the calling rank holds rows
+ * [g n/G, (g+1) n/G) of an n x n field (`local`, device, rows_local = n/G rows).  Row LCT
+ * into the all-to-all send layout (`send`: device [G][rows_local][n/G]), one all-to-all
+ * over the caller's NCCL communicator (`nccl_comm` = an ncclComm_t; grouped
+ * ncclSend/ncclRecv on `stream`), then the column LCT of the received row-major
+ * [n][n/G] slab in place (`slab`, device; `workspace`: n*n/G elements or NULL).
+ * The result stays column-sharded: `slab` holds columns [g n/G, (g+1) n/G) of the
+ * 2-D transform.  nccl_comm == NULL: one rank, no exchange (send unused).  n/G a power of two.
+ * NCCL is resolved at run time from the caller's process (no link dependency).
+ * Composition of fast_lct (xft/lct.py:168-208) along both axes. */
+int xft_lct2d_sharded(const void* local, void* slab, void* send, int64_t rows_local, int64_t n, int dtype,
+                      const double* abcd_row, const double* abcd_col, void* nccl_comm, void* workspace,
+                      void* stream);
+
 /* Column LCT of a [n_rows][n_cols] slab with row stride ld (device in/out,
  * abcd on the host): the second axis of the separable 2-D LCT and the receive
  * side of the sharded 2-D transform.  In place allowed.  `workspace`: n_rows*ld
@@ -204,6 +227,10 @@ int xft_validate_b_zero(const double* abcd, int64_t count, int64_t stride, doubl
 /* out = L in, L = dense_lct_matrix(n, abcd) (xft/dense.py:230-249); abcd == NULL: the
  * scaled Fourier matrix F (xft/kernel.py:68-80).  abcd on the host. */
 int xft_dense_lct_apply(const void* in, void* out, int64_t batch, int64_t n, const double* abcd_host, void* stream);
+/* out[j] = sum_k e^{sign 2 pi i (jk mod n)/n} in[k], the quadratic-time DFT oracle; replaces
+ * naive_dft (xft/fftcore.py:122-137): sign +-1 (else XFT_EPARAM), 1 <= n <= 4096 (else
+ * XFT_EINVALID_SIZE, the reference's _NAIVE_CAP). */
+int xft_naive_dft(const void* in, void* out, int64_t batch, int64_t n, int sign, void* stream);
 /* out = (K_z(x_j, x_k) dx) in, frft_matrix_asymptotic (xft/dense.py:122-151); z host (stride 0|2). */
 int xft_dense_mehler_apply(const void* in, void* out, int64_t batch, int64_t n, const double* z_host,
                            int64_t z_stride, void* stream);

@@ -38,6 +38,7 @@ _SIGS = {
     "xft_prepare": ([_i64, ctypes.c_int], ctypes.c_int),
     "xft_validate_lct_params": ([_vp, _i64, _i64, ctypes.c_int, ctypes.c_double, ctypes.POINTER(_i64)], ctypes.c_int),
     "xft_lct": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, ctypes.c_int, _vp], ctypes.c_int),
+    "xft_lct_checked": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, ctypes.c_int, _vp, _vp], ctypes.c_int),
     "xft_dft": ([_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
     "xft_scaled_fourier": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
     "xft_lct_host": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_double],
@@ -50,6 +51,7 @@ _SIGS = {
     "xft_mehler_plan_destroy": ([_vp], ctypes.c_int),
     "xft_release_caches": ([], ctypes.c_int),
     "xft_lct2d": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "xft_lct2d_sharded": ([_vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "xft_transpose": ([_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
     "xft_lct_columns": ([_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
     "xft_lct_rows_packed": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, ctypes.c_int, _i64, _vp], ctypes.c_int),
@@ -60,6 +62,7 @@ _SIGS = {
     "xft_validate_b_zero": ([_vp, _i64, _i64, ctypes.c_double, ctypes.POINTER(_i64)], ctypes.c_int),
     "xft_dense_lct_apply": ([_vp, _vp, _i64, _i64, _vp, _vp], ctypes.c_int),
     "xft_dense_mehler_apply": ([_vp, _vp, _i64, _i64, _vp, _i64, _vp], ctypes.c_int),
+    "xft_naive_dft": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
     "xft_dense_entries": ([_vp, _i64, ctypes.c_int, _vp, _vp], ctypes.c_int),
 }
 

@@ -42,13 +42,43 @@ struct LaunchArgs {
   int seg_log2w = 0;        // segmented (all-to-all send) output layout
   long long seg_stride = 0;  // 0: natural rows
   PeerTable peers{};         // peer-store output (count > 0)
+  unsigned long long* bad = nullptr;  // non-finite input report (xft_lct_checked)
 };
+
+// smallest row index holding a non-finite sample -> atomicMin(*bad): the
+// stand-alone check for the row paths whose kernels do not fuse it (short rows,
+// chirp-z, four-step); the pipelined row kernel checks inside its loads
+template <class C>
+__global__ void __launch_bounds__(256) nonfinite_rows_kernel(const C* __restrict__ in, long long batch, long long n,
+                                                            unsigned long long* bad) {
+  const long long total = batch * n;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < total; i += (long long)gridDim.x * 256) {
+    if (nonfinite_key(in[i]) == 0) atomicMin(bad, (unsigned long long)(i / n));
+  }
+}
+
+int scan_nonfinite(const void* in, long long batch, long long n, int dtype, unsigned long long* bad, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long want = (batch * n + 255) / 256;
+  const unsigned grid = (unsigned)(want < 8ll * sms ? (want < 1 ? 1 : want) : 8ll * sms);
+  if (dtype == XFT_C64)
+    nonfinite_rows_kernel<float2><<<grid, 256, 0, st>>>(static_cast<const float2*>(in), batch, n, bad);
+  else
+    nonfinite_rows_kernel<double2><<<grid, 256, 0, st>>>(static_cast<const double2*>(in), batch, n, bad);
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
 
 using LaunchFn = int (*)(const LaunchArgs&);
 
 // single-pass sizes (n <= radix): one register DFT per thread, no exchange
 template <class C, int L, int MODE, int SIGN>
 int launch_small(const LaunchArgs& a) {
+  if (a.bad) {
+    int rc = scan_nonfinite(a.in, a.batch, 1 << L, sizeof(C) == 8 ? XFT_C64 : XFT_C128, a.bad, a.st);
+    if (rc) return rc;
+  }
   using Cfg = RowCfg<C, L, (1 << L), MODE, SIGN>;
   auto kern = xft_rows_kernel<Cfg>;
   const long long grid = (a.batch + Cfg::ROWS - 1) / Cfg::ROWS;
@@ -145,6 +175,7 @@ int launch_pipe(const LaunchArgs& a) {
   kc.cnred = (long long)(((__int128)((1 << L) - 1) * ((1 << L) - 1)) % (4 * (__int128)(1 << L)));
   kc.log2n = L;
   kc.flags = a.flags;
+  kc.bad = a.bad;
   kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
       static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
       static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc, a.seg_log2w,
@@ -180,12 +211,16 @@ int log2_exact(int64_t n) {
 
 int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64_t n, int dtype,
              const double* abcd, int64_t stride, Abcd uni, int flags, cudaStream_t st, int seg_log2w = 0,
-             long long seg_stride = 0, const PeerTable* peers = nullptr) {
+             long long seg_stride = 0, const PeerTable* peers = nullptr, unsigned long long* bad = nullptr) {
   if (n < 1) return XFT_EINVALID_SIZE;
   if (batch < 0) return XFT_EINVALID_SIZE;
   if (dtype != XFT_C64 && dtype != XFT_C128) return XFT_EPARAM;
   if (batch == 0) return XFT_OK;
   const int l = log2_exact(n);
+  if (bad && (l < 0 || l > (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128))) {
+    const int rc = scan_nonfinite(in, batch, n, dtype, bad, st);
+    if (rc) return rc;
+  }
   if (l < 0) {  // not a power of two: chirp-z route (xft/fftcore.py:84-100)
     const double u4[4] = {uni.a, uni.b, uni.c, uni.d};
     return run_chirpz(mode, sign, in, out, batch, n, dtype, abcd, stride, u4, flags, st);
@@ -197,6 +232,7 @@ int run_rows(int mode, int sign, const void* in, void* out, int64_t batch, int64
   if ((seg_stride || peers) && (1 << l) <= pipe_radix(dtype, l))
     return XFT_ENOTSUP;  // segmented / peer epilogues live in the pipelined row kernel
   LaunchArgs a{in, out, (long long)batch, abcd, (long long)stride, uni, {}, flags, st};
+  a.bad = bad;
   a.seg_log2w = seg_log2w;
   a.seg_stride = seg_stride;
   if (seg_stride && (seg_log2w < 0 || seg_log2w > l || mode != MODE_LCT)) return XFT_EPARAM;
@@ -356,6 +392,17 @@ int xft_lct(const void* in, void* out, int64_t batch, int64_t n, int dtype, cons
             int flags, void* stream) {
   return run_rows(MODE_LCT, -1, in, out, batch, n, dtype, abcd, abcd_stride, Abcd{0, 0, 0, 0}, flags,
                   static_cast<cudaStream_t>(stream));
+}
+
+int xft_lct_checked(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd,
+                    int64_t abcd_stride, int flags, int64_t* bad_row, void* stream) {
+  if (!bad_row) return XFT_EPARAM;
+  auto st = static_cast<cudaStream_t>(stream);
+  // sentinel: INT64_MAX (no offending row); the kernels atomicMin row indices into it
+  if (cudaMemsetAsync(bad_row, 0xff, sizeof(int64_t), st) != cudaSuccess) return XFT_ECUDA;
+  if (cudaMemsetAsync(reinterpret_cast<char*>(bad_row) + 7, 0x7f, 1, st) != cudaSuccess) return XFT_ECUDA;
+  return run_rows(MODE_LCT, -1, in, out, batch, n, dtype, abcd, abcd_stride, Abcd{0, 0, 0, 0}, flags, st, 0, 0,
+                  nullptr, reinterpret_cast<unsigned long long*>(bad_row));
 }
 
 int xft_dft(const void* in, void* out, int64_t batch, int64_t n, int sign, int dtype, void* stream) {

@@ -41,6 +41,8 @@ struct DenseLct {
   double2 rnorm;  // 1 / sqrt(2 pi i b)
   double2 cn;     // C(n)
   int lct;        // 0: plain scaled Fourier matrix F
+  int plain;      // 1: the bare DFT kernel e^{sign 2 pi i (jk mod n)/n} (naive_dft): no p, no chirps, C = 1
+  int sign;       // DFT sign of w (the LCT / F paths use DFT_SIGN = -1)
 };
 
 __global__ void dense_vectors_kernel(DenseLct q, long long n, double2* ic, double2* oc, double2* p, double2* w) {
@@ -57,8 +59,8 @@ __global__ void dense_vectors_kernel(DenseLct q, long long n, double2* ic, doubl
     const long long red = (long long)(((__int128)(n - 1) * k) % (2 * (__int128)n));
     double s, c;
     sincospi((double)red / (double)n, &s, &c);
-    p[k] = make_double2(c, s);
-    sincospi(-2.0 * (double)k / (double)n, &s, &c);  // w^m = exp(-2 pi i m / n)
+    p[k] = q.plain ? make_double2(1.0, 0.0) : make_double2(c, s);
+    sincospi(2.0 * q.sign * (double)k / (double)n, &s, &c);  // w^m = exp(sign 2 pi i m / n)
     w[k] = make_double2(c, s);
   }
 }
@@ -186,6 +188,7 @@ DenseLct dense_lct_params(int64_t n, const double* abcd) {
   DenseLct q{};
   q.half = host_half_step(n);
   q.cn = host_kernel_prefactor(n);
+  q.sign = -1;
   q.lct = abcd != nullptr;
   if (abcd) {
     const double a = abcd[0], b = abcd[1], d = abcd[3];
@@ -249,6 +252,27 @@ int xft_dense_lct_apply(const void* in, void* out, int64_t batch, int64_t n, con
   int rc = s.alloc(n);
   if (rc) return rc;
   const DenseLct q = dense_lct_params(n, abcd_host);
+  dense_vectors_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(q, n, s.ic, s.oc, s.p, s.w);
+  constexpr int TJ = 32;
+  dim3 grid((unsigned)((n + TJ - 1) / TJ), (unsigned)batch);
+  dense_lct_apply_kernel<TJ><<<grid, 256, 2048 * sizeof(double2), st>>>(
+      static_cast<const double2*>(in), static_cast<double2*>(out), n, s.ic, s.oc, s.p, s.w, q.cn);
+  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+}
+
+int xft_naive_dft(const void* in, void* out, int64_t batch, int64_t n, int sign, void* stream) {
+  if (sign != 1 && sign != -1) return XFT_EPARAM;          // xft/fftcore.py:125-126
+  if (n < 1 || batch < 0) return XFT_EINVALID_SIZE;        // 129-130
+  if (n > MAX_DENSE_N) return XFT_EINVALID_SIZE;           // _NAIVE_CAP, 131-132
+  if (batch == 0) return XFT_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  Scratch s(st);
+  int rc = s.alloc(n);
+  if (rc) return rc;
+  DenseLct q = dense_lct_params(n, nullptr);
+  q.plain = 1;
+  q.sign = sign;
+  q.cn = make_double2(1.0, 0.0);
   dense_vectors_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(q, n, s.ic, s.oc, s.p, s.w);
   constexpr int TJ = 32;
   dim3 grid((unsigned)((n + TJ - 1) / TJ), (unsigned)batch);

@@ -152,7 +152,18 @@ struct RowConst {  // per-launch constants (host computed)
   long long cnred;  // (n-1)^2 mod 4n   (arg C(n) = -pi red / (2n))
   int log2n;
   int flags;
+  unsigned long long* bad = nullptr;  // non-null: atomicMin'd with every row holding a non-finite input
 };
+
+// 0 iff some component of x is Inf/NaN (all-ones exponent), two integer ops per component
+__device__ __forceinline__ unsigned nonfinite_key(double2 x) {
+  const unsigned e = 0x7ff00000u;
+  return min(~(unsigned)__double2hiint(x.x) & e, ~(unsigned)__double2hiint(x.y) & e);
+}
+__device__ __forceinline__ unsigned nonfinite_key(float2 x) {
+  const unsigned e = 0x7f800000u;
+  return min(~__float_as_uint(x.x) & e, ~__float_as_uint(x.y) & e);
+}
 
 __device__ __forceinline__ unsigned long long frac_q64(double v) {
   double f = v - floor(v);
@@ -1090,6 +1101,16 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
                      ptab, tab);
     } else {
       pre_multiply<Cfg>(v, rs, j, rc, tc, kc, ptab, tab);
+    }
+    // the reference rejects non-finite samples (xft/lct.py:125-126): when the
+    // caller asks (kc.bad), the pre-multiplied samples are checked right here --
+    // a unit-modulus pre-multiplier keeps Inf/NaN non-finite -- two integer ops
+    // per component, no extra HBM or shared-memory traffic
+    if (kc.bad != nullptr) {
+      unsigned fin = ~0u;
+#pragma unroll
+      for (int s = 0; s < Cfg::E; ++s) fin = min(fin, nonfinite_key(v[s]));
+      if (fin == 0 && tile * ROWS + lrow < batch) atomicMin(kc.bad, (unsigned long long)(tile * ROWS + lrow));
     }
 
     // runs right after the first exchange barrier of this tile

@@ -15,7 +15,9 @@ import numpy as np
 from . import ops
 from .errors import InvalidSizeError, ParameterError, ShapeError
 
-__all__ = ["DftPlan", "plan_dft", "apply_dft"]
+__all__ = ["DftPlan", "plan_dft", "apply_dft", "naive_dft"]
+
+NAIVE_CAP = 4096  # xft/fftcore.py:21
 
 
 class DftPlan:
@@ -62,3 +64,29 @@ def apply_dft_batch(plan: DftPlan, values):
     if values.shape[-1] != plan.n:
         raise ShapeError(f"expected rows of length {plan.n}, got {tuple(values.shape)}")
     return ops.dft_rows(values, plan.direction_sign)
+
+
+def naive_dft(v, direction_sign: int) -> np.ndarray:
+    """Quadratic-time DFT oracle (reference: xft/fftcore.py:122-137), on the GPU.
+
+    out[j] = sum_k exp(sign 2 pi i ((j k) mod n) / n) v[k], evaluated entry by
+    entry (``xft_naive_dft``: no FFT, shares nothing with the fast path), same
+    checks and order as the reference: sign, empty input, the n <= 4096 cap.
+    """
+    from . import _native
+
+    if direction_sign not in (1, -1):
+        raise ParameterError(f"direction_sign must be +1 or -1, got {direction_sign!r}")
+    v = np.asarray(v, dtype=complex)
+    n = v.shape[0]
+    if n < 1:
+        raise InvalidSizeError("empty input")
+    if n > NAIVE_CAP:
+        raise InvalidSizeError(f"naive DFT capped at n={NAIVE_CAP} (got {n})")
+    torch = ops._torch()
+    t = ops.aligned(torch.from_numpy(np.ascontiguousarray(v.reshape(1, n))).to("cuda"))
+    out = torch.empty_like(t)
+    with torch.cuda.device(t.device):
+        _native.call("xft_naive_dft", t.data_ptr(), out.data_ptr(), 1, n, int(direction_sign),
+                     ops._stream_ptr(t.device))
+    return out[0].cpu().numpy()

@@ -126,7 +126,9 @@ def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, co
     rank's symmetric-memory receive slab over NVLink (no separate collective,
     ``xft_lct_rows_peers``), two device-side barriers, column pass in place.
     The p2p result is that persistent slab: the next p2p call of the same shape
-    overwrites it.
+    overwrites it.  "capi" -- the whole sharded transform through the C ABI
+    (``xft_lct2d_sharded``) on the process group's own NCCL communicator: the
+    route a non-torch caller takes with its ncclComm_t.
     """
     import torch
     import torch.distributed as dist
@@ -145,8 +147,20 @@ def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, co
         rows_to_peers(local, abcd_row, list(hdl.buffer_ptrs), rank * rl)
         hdl.barrier()  # every rank's stores into this slab have landed
         return (col_fn or columns_inplace)(slab, abcd_col)
+    if transport == "capi":
+        pg = group if group is not None else dist.group.WORLD
+        comm = pg._get_backend(local.device)._comm_ptr()
+        local = ops.aligned(local)
+        send = ops.check_out(None if buffers is None else buffers[0], local, (world, rl, nc))
+        slab = ops.check_out(None if buffers is None else buffers[1].view(n, nc), local, (n, nc))
+        ws = torch.empty((n, nc), dtype=local.dtype, device=local.device) if n > 1024 else None
+        with torch.cuda.device(local.device):
+            _native.call("xft_lct2d_sharded", local.data_ptr(), slab.data_ptr(), send.data_ptr(), rl, n,
+                         ops._dtype_code(local), _abcd4(abcd_row).ctypes.data, _abcd4(abcd_col).ctypes.data,
+                         int(comm), None if ws is None else ws.data_ptr(), ops._stream_ptr(local.device))
+        return slab
     if transport != "nccl":
-        raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        raise ValueError(f"transport must be 'nccl', 'p2p' or 'capi', got {transport!r}")
     row_fn = row_fn or (lambda x, p, w: rows_packed(x, p, w, out=None if buffers is None else buffers[0]))
     col_fn = col_fn or columns_inplace
     send = row_fn(local, abcd_row, world)

@@ -111,12 +111,15 @@ def validate_abcd_host(abcd: np.ndarray, check_unimodular=True, tol=UNIMODULAR_T
 
 
 def lct_rows(values, abcd, *, bare_fourier=False, out=None, validate=True,
-             check_unimodular=True, tol=UNIMODULAR_TOL):
+             check_unimodular=True, tol=UNIMODULAR_TOL, check_finite=False):
     """Batched fast LCT of the rows of ``values`` ([B, n] complex64/complex128, CUDA).
 
     ``abcd``: 4 numbers (one quadruple for every row), a [B, 4] array, or a
     [B, 4] float64 CUDA tensor (per-row parameters, e.g. FrFT angles).
     Reference semantics: fast_lct (xft/lct.py:168-208) applied to every row.
+    ``check_finite``: the reference's Signal check (xft/lct.py:125-126) for the
+    whole batch, fused into the row kernel (``xft_lct_checked``); raises
+    ParameterError naming the first non-finite row (this synchronises the stream).
     """
     torch = _torch()
     v = _rows_view(values)
@@ -136,8 +139,16 @@ def lct_rows(values, abcd, *, bare_fourier=False, out=None, validate=True,
     out = check_out(out, v)
     flags = _native.FLAG_BARE_FOURIER if bare_fourier else 0
     with torch.cuda.device(v.device):
-        _native.call("xft_lct", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v),
-                     p_dev.data_ptr(), stride, flags, _stream_ptr(v.device))
+        if check_finite:
+            bad = torch.empty(1, dtype=torch.int64, device=v.device)
+            _native.call("xft_lct_checked", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v),
+                         p_dev.data_ptr(), stride, flags, bad.data_ptr(), _stream_ptr(v.device))
+            first = int(bad.item())
+            if first < B:
+                raise ParameterError(f"signal values must be finite (row {first})")
+        else:
+            _native.call("xft_lct", v.data_ptr(), out.data_ptr(), B, n, _dtype_code(v),
+                         p_dev.data_ptr(), stride, flags, _stream_ptr(v.device))
     # p_dev may be released now: the caching allocator only reuses its block
     # in order on this same stream.
     return out

@@ -275,3 +275,28 @@ def test_lct2d_golden(torch, X, golden):
     f = dev(torch, golden["lct2d_in"])
     got = lct2d.lct2d(f, (1.0, 0.25, 0.0, 1.0), (1.0, 0.25, 0.0, 1.0)).cpu().numpy()
     assert rel_l2(got, golden["lct2d_out"]) <= TOL128
+
+
+@pytest.mark.parametrize("n", [16, 1000, 4096, 8192, 16384, 32768])
+@pytest.mark.parametrize("dt", ["c64", "c128"])
+def test_nonfinite_rows_reported(torch, n, dt):
+    """check_finite: the reference's Signal check (xft/lct.py:125-126) on a batch -- fused into the
+    pipelined row kernel, a pre-scan on the short-row / chirp-z / four-step paths."""
+    from paper_0912_1379_b200 import ops
+    from paper_0912_1379_b200.errors import ParameterError
+
+    dtype = torch.complex64 if dt == "c64" else torch.complex128
+    rng = np.random.default_rng(n)
+    x = torch.from_numpy(rng.normal(size=(12, n)) + 1j * rng.normal(size=(12, n))).to(dtype).cuda()
+    p = (0.6, 0.8, -0.8, 0.6)
+    ref = ops.lct_rows(x, p)
+    assert torch.equal(ops.lct_rows(x, p, check_finite=True), ref)  # finite batch: same result
+    big = x.clone()
+    big[3, 7] = complex(1e300, -1e300) if dt == "c128" else complex(1e30, -1e30)  # finite: accepted
+    ops.lct_rows(big, p, check_finite=True)
+    for bad_val, rows in ((float("nan"), (9, 5)), (float("inf"), (11,)), (complex(0, -float("inf")), (2, 10))):
+        y = x.clone()
+        for r in rows:
+            y[r, (r * 37) % n] = bad_val
+        with pytest.raises(ParameterError, match=f"row {min(rows)}"):
+            ops.lct_rows(y, p, check_finite=True)

@@ -113,7 +113,8 @@ def test_columns_tall(torch, L2, R, dtype, tol, inplace):
 
 
 @pytest.mark.parametrize("n,dtype,tol", [(2048, np.complex64, 1e-6), (512, np.complex128, 1e-13)])
-def test_sharded_over_nccl_world1(torch, L2, tmp_path, n, dtype, tol):
+@pytest.mark.parametrize("transport", ["nccl", "capi"])
+def test_sharded_over_nccl_world1(torch, L2, tmp_path, n, dtype, tol, transport):
     """lct2d_sharded through a real NCCL process group (one rank: the only GPU of this box):
     packed row pass -> ncclAllToAll (all_to_all_single) -> column pass on the received slab."""
     import torch.distributed as dist
@@ -126,7 +127,7 @@ def test_sharded_over_nccl_world1(torch, L2, tmp_path, n, dtype, tol):
         rng = np.random.default_rng(17)
         f = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(dtype)
         ft = torch.from_numpy(f).cuda()
-        got = L2.lct2d_sharded(ft, ABCD5, (0.5, 1.5, -0.5, 0.5))
+        got = L2.lct2d_sharded(ft, ABCD5, (0.5, 1.5, -0.5, 0.5), transport=transport)
         torch.cuda.synchronize()
         ref = L2.lct2d(ft, ABCD5, (0.5, 1.5, -0.5, 0.5))
         assert got.shape == (n, n)
@@ -205,3 +206,46 @@ def test_slab_route_without_cluster_kernel(torch):
         _native._lib = saved
     err = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
     assert err <= 2e-6, err
+
+
+def test_capi_sharded_on_a_caller_owned_nccl_comm(torch, L2):
+    """xft_lct2d_sharded driven the way a non-torch caller drives it: its own ncclComm_t
+    (ncclGetUniqueId + ncclCommInitRank through ctypes, one rank), raw device pointers."""
+    import ctypes
+    import os
+
+    import nvidia.nccl
+
+    from paper_0912_1379_b200 import _native
+
+    nccl = ctypes.CDLL(os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2"))
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    torch.cuda.set_device(0)
+    assert nccl.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    try:
+        n = 2048
+        rng = np.random.default_rng(23)
+        f = torch.from_numpy((rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(np.complex64)).cuda()
+        send, slab, ws = torch.empty_like(f), torch.empty_like(f), torch.empty_like(f)
+        pr = np.array(ABCD5, dtype=np.float64)
+        pc = np.array((0.5, 1.5, -0.5, 0.5), dtype=np.float64)
+        s = torch.cuda.current_stream().cuda_stream
+        _native.call("xft_lct2d_sharded", f.data_ptr(), slab.data_ptr(), send.data_ptr(), n, n, _native.C64,
+                     pr.ctypes.data, pc.ctypes.data, comm.value, ws.data_ptr(), s)
+        torch.cuda.synchronize()
+        ref = L2.lct2d(f, ABCD5, (0.5, 1.5, -0.5, 0.5))
+        assert rel_l2(slab.cpu().numpy(), ref.cpu().numpy()) <= 1e-6
+        # shape contract: rows_local * world must tile n
+        from paper_0912_1379_b200.errors import ShapeError
+
+        with pytest.raises(ShapeError):
+            _native.call("xft_lct2d_sharded", f.data_ptr(), slab.data_ptr(), send.data_ptr(), n // 2, n,
+                         _native.C64, pr.ctypes.data, pc.ctypes.data, comm.value, ws.data_ptr(), s)
+    finally:
+        nccl.ncclCommDestroy(comm)
