@@ -300,3 +300,28 @@ def test_nonfinite_rows_reported(torch, n, dt):
             y[r, (r * 37) % n] = bad_val
         with pytest.raises(ParameterError, match=f"row {min(rows)}"):
             ops.lct_rows(y, p, check_finite=True)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 64, 600, 1000, 4096])
+@pytest.mark.parametrize("sign", [1, -1])
+def test_naive_dft_matches_oracle(torch, X, n, sign):
+    """naive_dft (xft/fftcore.py:122-137) on the GPU, entry by entry: vs the oracle's naive DFT and
+    the reference's known answers (pkg/tests/test_fftcore.py:45-52)."""
+    from oracle import xft_oracle as O
+
+    rng = np.random.default_rng(n + sign)
+    v = rng.normal(size=n) + 1j * rng.normal(size=n)
+    got = X.naive_dft(v, sign)
+    ref = O.naive_dft(v, sign)
+    assert rel_l2(got, ref) <= 1e-13
+    assert np.allclose(X.naive_dft(np.ones(2), -1), [2, 0], atol=1e-15)
+    assert np.allclose(X.naive_dft(np.array([0, 1, 0, 0]), -1), [1, -1j, -1, 1j], atol=1e-15)
+
+
+def test_naive_dft_errors(torch, X):
+    with pytest.raises(X.ParameterError):
+        X.naive_dft(np.ones(4), 0)
+    with pytest.raises(X.InvalidSizeError):
+        X.naive_dft(np.ones(0), 1)
+    with pytest.raises(X.InvalidSizeError):
+        X.naive_dft(np.ones(4097), 1)

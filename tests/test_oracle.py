@@ -109,3 +109,18 @@ def test_config5_shards_are_rows_of_the_full_draw():
     full = workloads.config5_field(n=128)
     part = workloads.config5_field(n=128, rows=32, row_start=64)
     assert np.array_equal(full[64:96], part)
+
+
+def test_hermite_table_matches_reference_rows():
+    """hermite_function_table (the config-3/4 input generator) == the reference's hermite_function_row,
+    bit for bit (fixture written by tests/golden/make_hermite_golden.py running xft/hermite.py:92-112)."""
+    import os
+
+    from paper_0912_1379_b200.hermite import hermite_function_row, hermite_function_table
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "hermite_rows.npz")
+    with np.load(path) as z:
+        for name in ("n1024_m21", "n16384_m31", "extra_m40"):
+            xs, psi = z[f"{name}_x"], z[f"{name}_psi"]
+            assert np.array_equal(hermite_function_table(psi.shape[0], xs), psi), name
+            assert np.array_equal(hermite_function_row(psi.shape[0], xs[3]), psi[:, 3])
