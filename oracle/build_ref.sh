@@ -3,7 +3,8 @@
 # oracle/_ref/ -- TEST/BENCH INFRASTRUCTURE ONLY.
 #
 # oracle/_ref/ is git-ignored (never committed) but not gpurun-ignored, so the
-# installed reference travels to the GPU box, where bench.py's CPU arms
+# installed reference (and a copy of its test suite, reference_tests/) travels
+# to the GPU box, where bench.py's CPU arms
 # (`--impl reference`, `cpu_baseline`) import it to time the reference's own
 # per-row fast_lct / fast_frft / mehler_kernel.  The product package never
 # imports it.  The reference has no native code, so "building" it is a plain
@@ -22,6 +23,9 @@ trap 'rm -rf "$TMP"' EXIT
 cp -r "$SRC" "$TMP/pkg"
 rm -rf "$DEST"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps --target "$DEST" "$TMP/pkg"
+# the reference's own test suite, run against the GPU package through tests/ref_shim
+# (tests/test_gpu_reference_suite.py); like the package, never committed
+cp -r "$SRC/tests" "$DEST/reference_tests"
 python - "$DEST" <<'EOF'
 import sys
 sys.path.insert(0, sys.argv[1])
