@@ -180,6 +180,9 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
 int xft_lct2d_sharded(const void* local, void* slab, void* send, int64_t rows_local, int64_t n, int dtype,
                       const double* abcd_row, const double* abcd_col, void* nccl_comm, void* workspace,
                       void* stream);
+/* The NCCL library xft_lct2d_sharded resolved in this process: its file path
+ * (path_len bytes incl. NUL) and ncclGetVersion code.  XFT_ENOTSUP: none loaded. */
+int xft_nccl_info(char* path, int path_len, int* version);
 
 /* Column LCT of a [n_rows][n_cols] slab with row stride ld (device in/out,
  * abcd on the host): the second axis of the separable 2-D LCT and the receive

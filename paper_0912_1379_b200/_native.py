@@ -52,6 +52,7 @@ _SIGS = {
     "xft_release_caches": ([], ctypes.c_int),
     "xft_lct2d": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp], ctypes.c_int),
     "xft_lct2d_sharded": ([_vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "xft_nccl_info": ([ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "xft_transpose": ([_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
     "xft_lct_columns": ([_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
     "xft_lct_rows_packed": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, ctypes.c_int, _i64, _vp], ctypes.c_int),

@@ -84,6 +84,9 @@
 #ifndef XFT_SPLIT
 #define XFT_SPLIT 1  // split next-row prefetch for single-row CTAs (see PipeCfg::SPLIT)
 #endif
+#ifndef XFT_SPLIT2
+#define XFT_SPLIT2 1  // ... also at two single-row CTAs per SM (c128 n = 4096: the spare ~36 KB per CTA)
+#endif
 
 #ifndef XFT_SKELETON
 #define XFT_SKELETON 0  // tuning only: 1 = exchanges without math, 2 = pure copy
@@ -450,9 +453,15 @@ struct PipeCfg {
   // SPLIT samples of the next row, loaded as soon as this row's input has been
   // read (first exchange barrier); the rest of the next row lands in the stage
   // once the last exchange has been read.  SPLIT is a multiple of TR.
-  static constexpr size_t SMEM_MAX = 232448 - 8192;  // 227 KB opt-in minus static shared memory
+  // Two resident CTAs per SM (c128 n = 4096) split the SM's 228 KB: each keeps
+  // its half minus the 1 KB per-CTA reservation and its static coefficient chunk.
+  static constexpr size_t STATIC_EST =
+      size_t(MODE == MODE_LCT ? (C128 ? XFT_C128_CH : 32) : 1) * ROWS * sizeof(Coef) + 8 * STAGES + 256;
+  static constexpr size_t SMEM_MAX = MINB_ == 1 ? 232448 - 8192  // 227 KB opt-in minus static shared memory
+                                                : 233472 / (MINB_ > 0 ? MINB_ : 1) - 1024 - STATIC_EST;
   static constexpr size_t MAIN = size_t(STAGES) * STAGE * sizeof(C) + TAB_BYTES;
-  static constexpr int SPLIT0 = (SPLITOK_ && ROWS == 1 && STAGES == 1 && MINB_ == 1 && XFT_SPLIT && SMEM_MAX > MAIN)
+  static constexpr int SPLIT0 = (SPLITOK_ && ROWS == 1 && STAGES == 1 && (MINB_ == 1 || (MINB_ == 2 && XFT_SPLIT2)) &&
+                                 XFT_SPLIT && SMEM_MAX > MAIN)
                                     ? int((SMEM_MAX - MAIN) / sizeof(C)) / TR * TR : 0;
   static constexpr int SPLIT = SPLIT0 < N ? SPLIT0 : 0;
   // Mirror lane map (row kernels, c128 LCT): lanes l and l^16 of a warp hold the

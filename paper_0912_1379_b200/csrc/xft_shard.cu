@@ -24,12 +24,14 @@ typedef int (*NcclGroupFn)();
 typedef int (*NcclP2PFn)(const void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*NcclRecvFn)(void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*NcclCommIntFn)(const void*, int*);
+typedef int (*NcclVersionFn)(int*);
 
 struct Nccl {
   NcclGroupFn group_start = nullptr, group_end = nullptr;
   NcclP2PFn send = nullptr;
   NcclRecvFn recv = nullptr;
   NcclCommIntFn count = nullptr, rank = nullptr;
+  NcclVersionFn version = nullptr;
   bool ok = false;
 };
 
@@ -49,6 +51,7 @@ const Nccl& nccl() {
     n.recv = reinterpret_cast<NcclRecvFn>(dlsym(h, "ncclRecv"));
     n.count = reinterpret_cast<NcclCommIntFn>(dlsym(h, "ncclCommCount"));
     n.rank = reinterpret_cast<NcclCommIntFn>(dlsym(h, "ncclCommUserRank"));
+    n.version = reinterpret_cast<NcclVersionFn>(dlsym(h, "ncclGetVersion"));
     n.ok = n.group_start && n.group_end && n.send && n.recv && n.count && n.rank;
   });
   return n;
@@ -66,6 +69,25 @@ int log2_pow2(int64_t v) {
 }  // namespace
 
 extern "C" {
+
+int xft_nccl_info(char* path, int path_len, int* version) {
+  const Nccl& nc = nccl();
+  if (!nc.ok) return XFT_ENOTSUP;
+  if (version) {
+    *version = 0;
+    if (nc.version) nc.version(version);
+  }
+  if (path && path_len > 0) {
+    Dl_info info{};
+    path[0] = 0;
+    if (dladdr(reinterpret_cast<void*>(nc.send), &info) && info.dli_fname) {
+      int i = 0;
+      for (; info.dli_fname[i] && i < path_len - 1; ++i) path[i] = info.dli_fname[i];
+      path[i] = 0;
+    }
+  }
+  return XFT_OK;
+}
 
 int xft_lct2d_sharded(const void* local, void* slab, void* send, int64_t rows_local, int64_t n, int dtype,
                       const double* abcd_row, const double* abcd_col, void* nccl_comm, void* workspace,
