@@ -85,7 +85,7 @@
 #define XFT_SPLIT 1  // split next-row prefetch for single-row CTAs (see PipeCfg::SPLIT)
 #endif
 #ifndef XFT_SPLIT2
-#define XFT_SPLIT2 1  // ... also at two single-row CTAs per SM (c128 n = 4096: the spare ~36 KB per CTA)
+#define XFT_SPLIT2 0  // 1: also at two single-row CTAs per SM (c128 n = 4096, the spare ~36 KB per CTA): A/B 121.0 vs 119.2 us, off
 #endif
 
 #ifndef XFT_SKELETON

@@ -97,6 +97,40 @@ def columns_inplace(slab, abcd_col, workspace=None):
 
 
 _P2P = {}  # (group, n, dtype, device) -> (symmetric receive slab, its rendezvous handle)
+_COMMS = {}  # (group, device) -> ncclComm_t of the "capi" transport
+
+
+def _capi_comm(group, device):
+    """An NCCL communicator of our own over ``group``'s ranks, made the way a non-torch caller makes
+    one (ncclGetUniqueId on rank 0, broadcast, ncclCommInitRank), for ``xft_lct2d_sharded``."""
+    import ctypes
+    import os
+
+    import nvidia.nccl
+    import torch
+    import torch.distributed as dist
+
+    key = (id(group), str(device))
+    if key not in _COMMS:
+        nccl = ctypes.CDLL(os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2"))
+
+        class UniqueId(ctypes.Structure):
+            _fields_ = [("internal", ctypes.c_char * 128)]
+
+        uid = UniqueId()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if rank == 0 and nccl.ncclGetUniqueId(ctypes.byref(uid)) != 0:
+            raise RuntimeError("ncclGetUniqueId failed")
+        box = [bytes(uid.internal) if rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        uid.internal = box[0]
+        comm = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            if nccl.ncclCommInitRank(ctypes.byref(comm), world, uid, rank) != 0:
+                raise RuntimeError("ncclCommInitRank failed")
+        _COMMS[key] = comm.value
+    return _COMMS[key]
 
 
 def _p2p_slab(group, n, nc, dtype, device):
@@ -127,8 +161,9 @@ def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, co
     ``xft_lct_rows_peers``), two device-side barriers, column pass in place.
     The p2p result is that persistent slab: the next p2p call of the same shape
     overwrites it.  "capi" -- the whole sharded transform through the C ABI
-    (``xft_lct2d_sharded``) on the process group's own NCCL communicator: the
-    route a non-torch caller takes with its ncclComm_t.
+    (``xft_lct2d_sharded``) on an NCCL communicator of its own over the group's
+    ranks (made with the plain NCCL API): the route a non-torch caller takes
+    with its ncclComm_t.
     """
     import torch
     import torch.distributed as dist
@@ -148,15 +183,15 @@ def lct2d_sharded(local, abcd_row, abcd_col=None, *, group=None, row_fn=None, co
         hdl.barrier()  # every rank's stores into this slab have landed
         return (col_fn or columns_inplace)(slab, abcd_col)
     if transport == "capi":
-        pg = group if group is not None else dist.group.WORLD
-        comm = pg._get_backend(local.device)._comm_ptr()
+        comm = _capi_comm(group, local.device)
         local = ops.aligned(local)
         send = ops.check_out(None if buffers is None else buffers[0], local, (world, rl, nc))
         slab = ops.check_out(None if buffers is None else buffers[1].view(n, nc), local, (n, nc))
         ws = torch.empty((n, nc), dtype=local.dtype, device=local.device) if n > 1024 else None
+        pr, pc = _abcd4(abcd_row), _abcd4(abcd_col)  # held: the call reads them through raw pointers
         with torch.cuda.device(local.device):
             _native.call("xft_lct2d_sharded", local.data_ptr(), slab.data_ptr(), send.data_ptr(), rl, n,
-                         ops._dtype_code(local), _abcd4(abcd_row).ctypes.data, _abcd4(abcd_col).ctypes.data,
+                         ops._dtype_code(local), pr.ctypes.data, pc.ctypes.data,
                          int(comm), None if ws is None else ws.data_ptr(), ops._stream_ptr(local.device))
         return slab
     if transport != "nccl":

@@ -15,6 +15,7 @@ from _variant import use_variant  # noqa: E402
 tag = use_variant()
 sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
 import xft as R  # noqa: E402  (the reference, for the oracle and its own error)
+import xft.calibration  # noqa: E402,F401
 
 from paper_0912_1379_b200 import lct as L  # noqa: E402
 from paper_0912_1379_b200.hermite import asymptotic_zeros  # noqa: E402
