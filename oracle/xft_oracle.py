@@ -215,6 +215,22 @@ def scaled_fourier_rows(v: np.ndarray) -> np.ndarray:
     return kernel_prefactor(n) * (p * dft_rows(p * v, DFT_SIGN))
 
 
+def dense_lct_rows(abcd, n: int, rows) -> np.ndarray:
+    """Selected rows j of the dense LCT matrix, in the reference's operation order
+    (dense_lct_matrix, xft/dense.py:162-171; scaled_fourier_matrix, xft/kernel.py:68-80):
+    L[j, k] = oc_j * (C(n) * (p_j * e^{-2 pi i (jk mod n)/n} * p_k)) * ic_k.
+    Any n (the reference caps the materialised matrix at 4096; one row is O(n))."""
+    a, b, _c, d = (float(t) for t in abcd)
+    js = np.asarray(rows, dtype=np.int64)
+    x = asymptotic_nodes(n)
+    y = (4.0 * b / np.pi) * x
+    k = np.arange(n, dtype=np.int64)
+    dft = np.exp(DFT_SIGN * 2j * np.pi * ((js[:, None] * k[None, :]) % n) / n)
+    p = boundary_phase(n)
+    f = kernel_prefactor(n) * (p[js][:, None] * dft * p[None, :])
+    return output_chirp(d, b, y)[js][:, None] * f * input_chirp(a, b, x)[None, :]
+
+
 def lct2d(abcd_row, abcd_col, field: np.ndarray) -> np.ndarray:
     """Separable 2-D LCT: fast_lct along axis 1, then along axis 0.
 

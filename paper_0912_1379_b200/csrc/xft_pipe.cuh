@@ -210,6 +210,9 @@ __device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd
 #ifndef XFT_C128_WALK
 #define XFT_C128_WALK 1  // 0: every c128 chirp through the per-element table path (modes 3/4)
 #endif
+#ifndef XFT_WALK_MIN_LOG2N
+#define XFT_WALK_MIN_LOG2N 11  // c128 rows shorter than 2^11 use the per-element table path (accuracy)
+#endif
 #ifndef XFT_WALK_SMOOTH_BELOW
 #define XFT_WALK_SMOOTH_BELOW 2048.0  // rows with max |phase| below this skip the rounding corrections
 #endif
@@ -297,9 +300,14 @@ __device__ __forceinline__ void make_coef(Coef128& c, const double* p, const Abc
   const double pmax_in = fabs(c.cin) * x2 * x2;
   const double y2 = fabs(c.s4) * x2;
   const double pmax_out = fabs(c.cout) * y2 * y2;
-  auto mode_of = [](double pm) {
-    if (XFT_C128_WALK && pm < XFT_WALK_SMOOTH_BELOW) return 1;
-    if (XFT_C128_WALK && pm < 16777216.0) return 2;
+  // short rows (n < 2^XFT_WALK_MIN_LOG2N: latency-bound, never FP64-bound) take the
+  // exact per-element table path: the walk's accumulated rounding (~15 products)
+  // would double the reference's own error at n = 512 (its frozen figure-1
+  // threshold, xft/calibration.py:17-22: 2.84e-15 walked vs 1.35e-15 tabled)
+  const bool walk = XFT_C128_WALK && k.log2n >= XFT_WALK_MIN_LOG2N;
+  auto mode_of = [walk](double pm) {
+    if (walk && pm < XFT_WALK_SMOOTH_BELOW) return 1;
+    if (walk && pm < 16777216.0) return 2;
     return pm < 1e12 ? 3 : 4;
   };
   c.pre = (a != 0.0) ? mode_of(pmax_in) : 0;

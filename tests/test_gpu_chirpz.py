@@ -233,3 +233,23 @@ def test_mehler_config3_truth(torch, X):
     for i, r in enumerate(rows):
         truth = g[f"truth_{r}"]
         assert rel_l2(got[i, js], truth) <= 1e-12, (r, rel_l2(got[i, js], truth))
+
+
+@pytest.mark.slow
+def test_mehler_config3_every_row_against_dense_gpu_oracle(torch, X):
+    """All 1024 rows x 16384 outputs of config 3 against the entry-by-entry dense Mehler product
+    (``xft_dense_mehler_apply``: K_z(x_j, x_k) dx in the reference's operation order,
+    xft/dense.py:122-151; no FFT, nothing shared with the windowed Bluestein kernels)."""
+    from paper_0912_1379_b200 import dense, workloads
+
+    c3 = workloads.config3()
+    z = c3.extra["z"]
+    v = dev(torch, c3.values)
+    got = X.mehler_rows(v, z).cpu().numpy()
+    worst = []
+    for s in range(0, z.shape[0], 128):  # the dense product in blocks of rows (bounded memory)
+        ref = dense.dense_mehler_apply(v[s:s + 128], z[s:s + 128]).cpu().numpy()
+        for r in range(ref.shape[0]):
+            e = rel_l2(got[s + r], ref[r])
+            worst.append(e / _mehler_tol(z[s + r]))
+    assert max(worst) <= 1.0, (int(np.argmax(worst)), max(worst))

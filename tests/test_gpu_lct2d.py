@@ -249,3 +249,32 @@ def test_capi_sharded_on_a_caller_owned_nccl_comm(torch, L2):
                          _native.C64, pr.ctypes.data, pc.ctypes.data, comm.value, ws.data_ptr(), s)
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+@pytest.mark.slow
+def test_config5_256_rows_and_256_columns_independent(torch, L2):
+    """Config 5 at full size: 256 output columns and 256 output rows against an oracle that shares
+    nothing with the GPU path.  Output column c = fast_lct(F L[c, :]^T) and output row r =
+    fast_lct(L[r, :] F): the dense LCT rows L[j, :] restate xft/dense.py:162-171 exactly
+    (oracle.dense_lct_rows, pinned bit for bit to the reference's matrix), the contraction with the
+    c64-rounded field runs in complex128 (a plain ZGEMM), the final 1-D transform is the oracle's
+    fast_lct.  Tolerance: the complex64 bar (2e-5 per line)."""
+    from paper_0912_1379_b200 import workloads
+
+    n = 16384
+    field = workloads.config5_field(n)
+    ft = torch.from_numpy(field).cuda()
+    out = L2.lct2d(ft, ABCD5, ABCD5).cpu().numpy()
+    f128 = ft.to(torch.complex128)
+    del ft
+    rng = np.random.default_rng(55)
+    idx = np.unique(np.concatenate([[0, n // 2, n - 1], rng.choice(n, 253, replace=False)]))[:256]
+    Lsel = torch.from_numpy(O.dense_lct_rows(ABCD5, n, idx)).cuda()   # [256, n] rows of L
+    cols_in = (f128 @ Lsel.T).T.contiguous().cpu().numpy()             # [256, n]: F L[c, :]^T
+    rows_in = (Lsel @ f128).cpu().numpy()                              # [256, n]: L[r, :] F
+    del f128
+    _, want_cols = O.fast_lct_rows(ABCD5, cols_in)
+    _, want_rows = O.fast_lct_rows(ABCD5, rows_in)
+    for i, c in enumerate(idx):
+        assert rel_l2(out[:, c], want_cols[i]) <= 2e-5, ("column", c)
+        assert rel_l2(out[c, :], want_rows[i]) <= 2e-5, ("row", c)

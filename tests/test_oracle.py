@@ -124,3 +124,20 @@ def test_hermite_table_matches_reference_rows():
             xs, psi = z[f"{name}_x"], z[f"{name}_psi"]
             assert np.array_equal(hermite_function_table(psi.shape[0], xs), psi), name
             assert np.array_equal(hermite_function_row(psi.shape[0], xs[3]), psi[:, 3])
+
+
+def test_dense_lct_rows_matches_reference_matrix():
+    """dense_lct_rows (the full-size 2-D parity checker) == rows of the reference's dense_lct_matrix,
+    bit for bit (tests/golden/cli_golden.json: xft/dense.py dense_lct_matrix at n = 48)."""
+    import json
+    import os
+
+    from oracle import xft_oracle as O
+
+    gold = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cli_golden.json")))
+    d = gold["oracles"]["dense_L"]
+    n = d["n"]
+    L = (np.array(d["re"]) + 1j * np.array(d["im"])).reshape(n, n)
+    abcd = gold["oracles"]["closed_form"]["abcd"]  # the same parameters (make_cli_golden.py)
+    rows = [0, 5, 17, n - 1]
+    assert np.array_equal(O.dense_lct_rows(abcd, n, rows), L[rows])
