@@ -202,6 +202,12 @@ def make_workload(name: str, rows_override=None, rank=0, world=1, replicate=Fals
     raise SystemExit(f"unknown config {name}")
 
 
+def workload_config(cfg):
+    """The line's `config`: the workload and its size (same dict on both arms)."""
+    return dict(cfg, l2="inputs and outputs exceed L2 (126 MB) for configs 2-5; the GPU arm also rotates "
+                        "3 input/output sets")
+
+
 def samples_of(work):
     return sum(it.samples for it in work)
 
@@ -280,8 +286,8 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Msamples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded)",
-        "config": cfg,
+        "scaling": "strong", "vs_baseline": None, "dtype": DTYPE_OF(work),
+        "data": "synthetic (seeded, BASELINE config draw order)", "config": workload_config(cfg),
         "cpu_baseline": {"value": value, "unit": "Msamples/s", "cores": procs, "kind": kind,
                          "sample": f"{sample}; {src}; {procs}-process pool over shared memory"},
         "e2e": {"value": value, "unit": "Msamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -628,31 +634,31 @@ def run_ours(args, rank, world, local_rank):
         if c == "cfg5":
             cfgs[c]["transport"] = rec["transport"] if world > 1 else "single GPU (rows -> 8 slabs -> columns)"
     strong = args.config in ("cfg2", "cfg3", "cfg4") and world > 1
+    # `config` names the workload only (identical on the reference arm's line); how it ran is beside it
     line = {
         "metric": METRIC, "value": head["value"], "unit": "Msamples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
         "scaling": "strong" if args.config in ("cfg2", "cfg3", "cfg4") else "weak",
         "vs_baseline": None, "dtype": DTYPE_OF(work), "data": "synthetic (seeded, BASELINE config draw order)",
-        "config": dict(head["config"], l2="3 rotating input/output sets; each launch streams >= 2x L2 of cold data",
-                       parallelism=(f"rows sharded over {world} GPU(s) (rank r: rows [rB/N,(r+1)B/N)), "
-                                    "no collective" if args.config != "cfg5"
-                                    else f"row-sharded x{world}, " + ("row-kernel NVLink peer stores"
-                                                                      if head["transport"] == "p2p" and world > 1
-                                                                      else ("NCCL all_to_all_single" if world > 1
-                                                                            else "single GPU"))),
-                       timing=("CUDA graphs" if head["capturable"] else "direct launches")
-                       + (", step items on independent streams" if head["capturable"] and args.overlap
-                          and len(work) > 1 else "")),
+        "config": workload_config(head["config"]),
+        "parallelism": (f"rows sharded over {world} GPU(s) (rank r: rows [rB/N,(r+1)B/N)), no collective"
+                        if args.config != "cfg5"
+                        else f"row-sharded x{world}, " + ("row-kernel NVLink peer stores" if head["transport"] == "p2p"
+                                                           and world > 1 else ("NCCL all_to_all_single" if world > 1
+                                                                               else "single GPU"))),
+        "timing": ("CUDA graphs" if head["capturable"] else "direct launches")
+        + (", step items on independent streams" if head["capturable"] and args.overlap and len(work) > 1 else "")
+        + "; 3 rotating input/output sets",
         "roofline": roof, "per_dtype": per, "cpu_baseline": cpu, "e2e": head["e2e"],
         "gpu_launches": head["launches"], "clocks": head["clocks"],
     }
+    if strong:
+        line["shard_rows_per_rank"] = head["work"][0].values.shape[0]
     if cfgs:
         line["configs"] = cfgs
     if weak is not None:
         line["weak_scaling"] = {"value": weak["value"], "unit": "Msamples/s", "ms_per_step": weak["ms_per_step"],
                                 "what": f"every rank transforms the full {args.config} batch (replicated rows)"}
-    if strong:
-        line["config"]["shard_rows_per_rank"] = head["work"][0].values.shape[0]
     print(json.dumps(line), flush=True)
     del torch
 

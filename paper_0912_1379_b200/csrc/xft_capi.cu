@@ -176,11 +176,23 @@ int launch_pipe(const LaunchArgs& a) {
   kc.log2n = L;
   kc.flags = a.flags;
   kc.bad = a.bad;
-  kern<<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, a.st>>>(
-      static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch, a.abcd, a.stride, a.uni,
-      static_cast<const C*>(a.tb.tw), static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc, a.seg_log2w,
-      a.seg_stride, a.peers);
-  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+  // programmatic stream serialization: the next launch's CTAs may start their
+  // prologue while this grid's tail runs (the kernel waits before touching data)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = a.st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = XFT_PDL ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch,
+                                           a.abcd, (long long)a.stride, a.uni, static_cast<const C*>(a.tb.tw),
+                                           static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc, a.seg_log2w,
+                                           a.seg_stride, a.peers);
+  return e == cudaSuccess ? XFT_OK : XFT_ECUDA;
 }
 
 template <class C, int L, int MODE, int SIGN>

@@ -491,6 +491,16 @@ struct PipeCfg {
   static constexpr int MINB = MINB_;
 };
 
+#ifndef XFT_PDL
+#define XFT_PDL 1  // row kernels launched with programmatic stream serialization (griddepcontrol)
+#endif
+__device__ __forceinline__ void griddep_launch_dependents() {
+  if (XFT_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() {
+  if (XFT_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // padded exchange index: element a of a row lives at a + a/16
 __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 
@@ -1034,13 +1044,10 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   };
 
   // ---- prologue ----
-  if constexpr (Cfg::MODE == MODE_LCT && XFT_COEF_PREFETCH) {
-    // the first chunk's parameter rows: their global latency overlaps the table copy
-    if (abcd && tid < CH * ROWS) {
-      const long long row = ((long long)blockIdx.x + (long long)(tid / ROWS) * G) * ROWS + tid % ROWS;
-      if (row < batch) asm volatile("prefetch.global.L1 [%0];" ::"l"(abcd + row * abcd_stride));
-    }
-  }
+  // Programmatic dependent launch (XFT_PDL): the next launch on this stream may
+  // start its own prologue on SMs this grid frees; everything before
+  // griddep_wait() below touches only library-owned constant tables.
+  griddep_launch_dependents();
   if constexpr (XFT_TW_PREFETCH && Cfg::NPASS > 1) {
     // this thread's first-row twiddle entries (w and w^8 of every pass) into L1
 #pragma unroll
@@ -1059,6 +1066,15 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     const double2* g = static_cast<const double2*>(gtab);
     for (int m = tid; m < XFT_C128_TABCOPIES * C128_TABN; m += Cfg::THREADS)
       t[m] = g[XFT_C128_TABCOPIES == 8 ? m >> 3 : m];
+  }
+  // the caller's data (in, abcd, out) only after the previous grid on the stream is complete
+  griddep_wait();
+  if constexpr (Cfg::MODE == MODE_LCT && XFT_COEF_PREFETCH) {
+    // the first chunk's parameter rows: their global latency overlaps the barrier and first TMA issue
+    if (abcd && tid < CH * ROWS) {
+      const long long row = ((long long)blockIdx.x + (long long)(tid / ROWS) * G) * ROWS + tid % ROWS;
+      if (row < batch) asm volatile("prefetch.global.L1 [%0];" ::"l"(abcd + row * abcd_stride));
+    }
   }
   __syncthreads();
   long long tile = blockIdx.x;
