@@ -492,7 +492,7 @@ struct PipeCfg {
 };
 
 #ifndef XFT_PDL
-#define XFT_PDL 1  // row kernels launched with programmatic stream serialization (griddepcontrol)
+#define XFT_PDL 0  // 1: row kernels launched with programmatic stream serialization (A/B: c128 119.05 vs 119.3 us, c64 53.6 vs 52.6 us: off)
 #endif
 __device__ __forceinline__ void griddep_launch_dependents() {
   if (XFT_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -7,6 +7,10 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _variant import use_variant  # noqa: E402
+
+print("library:", use_variant())
 import torch  # noqa: E402
 
 from paper_0912_1379_b200 import dense, mehler, workloads  # noqa: E402
