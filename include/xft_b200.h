@@ -144,8 +144,10 @@ int xft_validate_mehler_z(const double* z, int64_t count, int64_t stride, int64_
 
 /* Caller-owned Mehler plan for one z array on the current device (the
  * analogue of holding frft_matrix_asymptotic's DenseTransform,
- * xft/dense.py:139-151): per-row parameters, size classes and row lists,
- * built once (validated like xft_mehler).  xft_mehler_planned applies it to a
+ * xft/dense.py:139-151): per-row parameters, size classes, row lists and every
+ * row's kernel spectrum FFT(h) (a function of z alone; sum over rows of M * 16
+ * bytes, M = the row's windowed convolution length <= 2^ceil(log2(2n-1))),
+ * built once on a private stream (validated like xft_mehler).  xft_mehler_planned applies it to a
  * [batch][n] complex128 batch (workspace as xft_mehler).  A plan is immutable and
  * may be used from several threads/streams at once; destroy it only when no
  * pending work or live CUDA graph uses it. */

@@ -257,14 +257,19 @@ struct MehlerPlan {
   OpMehlerRow* rows = nullptr;              // [batch] device
   int* list = nullptr;                      // [batch] device, rows grouped by class
   std::vector<std::pair<int, long long>> classes;  // (log2 M, count) in list order
+  // kernel spectra FFT(h) of every row ([class rows][M] per class, four-step classes in their
+  // permuted order): functions of z alone, computed once when the plan is built
+  double2* hspec = nullptr;
+  std::vector<size_t> hoff;  // element offset of each class in hspec
   int maxl = 0;
   ~MehlerPlan() {
-    if (rows || list) {
+    if (rows || list || hspec) {
       int cur = 0;
       cudaGetDevice(&cur);
       cudaSetDevice(dev);
       cudaFree(rows);
       cudaFree(list);
+      cudaFree(hspec);
       cudaSetDevice(cur);
     }
   }
@@ -382,15 +387,45 @@ int build_mehler_plan(int dev, int64_t batch, int64_t n, std::vector<double> zv,
     if (kv.first <= MAXL_C128) p->maxl = kv.first;
   }
   p->z = std::move(zv);
-  const bool ok = relaxed_capture([&]() {
-    return cudaMalloc(&p->rows, batch * sizeof(OpMehlerRow)) == cudaSuccess &&
-           cudaMalloc(&p->list, batch * sizeof(int)) == cudaSuccess &&
-           cudaMemcpy(p->rows, rows.data(), batch * sizeof(OpMehlerRow), cudaMemcpyHostToDevice) == cudaSuccess &&
-           cudaMemcpy(p->list, list.data(), batch * sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+  size_t hs_elems = 0;
+  for (const auto& cl : p->classes) {
+    p->hoff.push_back(hs_elems);
+    hs_elems += (size_t)cl.second << cl.first;
+  }
+  // the kernel spectra run on a private stream and are waited for here: plan creation is
+  // host-synchronous (like the uploads above) and stays outside any graph being captured
+  const int rc = relaxed_capture([&]() -> int {
+    if (cudaMalloc(&p->rows, batch * sizeof(OpMehlerRow)) != cudaSuccess ||
+        cudaMalloc(&p->list, batch * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&p->hspec, hs_elems * sizeof(double2)) != cudaSuccess ||
+        cudaMemcpy(p->rows, rows.data(), batch * sizeof(OpMehlerRow), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->list, list.data(), batch * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+      return XFT_ECUDA;
+    cudaStream_t ps = nullptr;
+    if (cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking) != cudaSuccess) return XFT_ECUDA;
+    int r = XFT_OK;
+    size_t off = 0;
+    for (size_t c = 0; c < p->classes.size() && !r; ++c) {
+      const auto& cl = p->classes[c];
+      if (cl.first <= MAXL_C128) {
+        OpMehlerSpec op;
+        op.rows = p->rows;
+        op.hscratch = p->hspec + p->hoff[c];
+        op.half = host_half_step(n);
+        op.n = (int)n;
+        r = blue<double2>(cl.first, nullptr, nullptr, cl.second, p->list + off, op, ps);
+      } else {
+        r = large_mehler_spectrum(cl.second, p->list + off, p->rows, cl.first, p->hspec + p->hoff[c], ps);
+      }
+      off += (size_t)cl.second;
+    }
+    if (cudaStreamSynchronize(ps) != cudaSuccess && !r) r = XFT_ECUDA;
+    cudaStreamDestroy(ps);
+    return r;
   });
-  if (!ok) {
+  if (rc) {
     cudaGetLastError();
-    return XFT_ECUDA;  // ~MehlerPlan frees what was allocated
+    return rc;  // ~MehlerPlan frees what was allocated
   }
   *out = std::move(p);
   return XFT_OK;
@@ -462,23 +497,24 @@ int mehler_run(const void* in, void* out, const MehlerPlan& plan, void* workspac
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t n = plan.n;
   int rc = XFT_OK;
-  // per launched CTA one kernel-spectrum row of the largest in-CTA class, then
-  // the four-step classes' spectrum + data rows (2 x count x M)
-  const size_t hs_bytes = (size_t)sms * 8 * ((size_t)1 << plan.maxl) * sizeof(double2);
+  // scratch: the four-step classes' data rows (count x M each); the kernel spectra are the plan's
   size_t all_bytes = 0;
   for (const auto& cl : plan.classes)
-    all_bytes += cl.first <= MAXL_C128 ? hs_bytes : 2 * (size_t)cl.second * ((size_t)1 << cl.first) * 16;
+    if (cl.first > MAXL_C128) all_bytes += (size_t)cl.second * ((size_t)1 << cl.first) * 16;
   OpMehler op;
   op.rows = plan.rows;
   op.half = host_half_step(n);
   op.n = (int)n;
   if (workspace) {  // caller scratch (xft_mehler_workspace_bytes): the classes one after another
-    op.hscratch = static_cast<double2*>(workspace);
     size_t off = 0;
-    for (const auto& cl : plan.classes) {
+    for (size_t c = 0; c < plan.classes.size(); ++c) {
+      const auto& cl = plan.classes[c];
       const long long cnt = cl.second;
-      rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan.list + off, op, st)
-                                 : run_large_mehler(in, out, cnt, plan.list + off, plan.rows, cl.first, n, st);
+      OpMehler oc = op;
+      oc.hscratch = plan.hspec + plan.hoff[c];
+      rc = cl.first <= MAXL_C128 ? blue<double2>(cl.first, in, out, cnt, plan.list + off, oc, st)
+                                 : run_large_mehler(in, out, cnt, plan.list + off, plan.rows, cl.first, n, st,
+                                                    workspace, plan.hspec + plan.hoff[c]);
       if (rc) return rc;
       off += cnt;
     }
@@ -488,7 +524,7 @@ int mehler_run(const void* in, void* out, const MehlerPlan& plan, void* workspac
   // (forked from and joined back to `st`, so the call stays stream-ordered and
   // graph-capturable) with its own scratch, and the small in-CTA classes fill
   // the SMs the four-step classes' short tile kernels leave idle.
-  char* base = static_cast<char*>(stream_scratch(dev, st, all_bytes));
+  char* base = static_cast<char*>(stream_scratch(dev, st, all_bytes > 0 ? all_bytes : 16));
   if (!base) return XFT_ECUDA;
   SideStreams& ss = side_streams(dev, st, (int)plan.classes.size());
   if (!ss.ok) return XFT_ECUDA;
@@ -506,12 +542,12 @@ int mehler_run(const void* in, void* out, const MehlerPlan& plan, void* workspac
     forked = c + 1;
     if (cl.first <= MAXL_C128) {
       OpMehler oc = op;
-      oc.hscratch = reinterpret_cast<double2*>(base + boff);
-      boff += hs_bytes;
+      oc.hscratch = plan.hspec + plan.hoff[c];
       rc = blue<double2>(cl.first, in, out, cnt, plan.list + off, oc, sc);
     } else {
-      rc = run_large_mehler(in, out, cnt, plan.list + off, plan.rows, cl.first, n, sc, base + boff);
-      boff += 2 * (size_t)cnt * ((size_t)1 << cl.first) * 16;
+      rc = run_large_mehler(in, out, cnt, plan.list + off, plan.rows, cl.first, n, sc, base + boff,
+                            plan.hspec + plan.hoff[c]);
+      boff += (size_t)cnt * ((size_t)1 << cl.first) * 16;
     }
     off += cnt;
   }
@@ -526,10 +562,10 @@ int mehler_run(const void* in, void* out, const MehlerPlan& plan, void* workspac
 extern "C" {
 
 int64_t xft_mehler_workspace_bytes(int64_t batch, int64_t n) {
-  // per resident CTA one kernel-spectrum row of the largest class + the row tables
+  // the four-step classes' data rows: at most every row at the largest convolution length
   int64_t m = 1;
   while (m < 2 * n - 1) m *= 2;
-  return (int64_t)148 * 8 * m * 16 + batch * (int64_t)(sizeof(OpMehlerRow) + sizeof(int)) + 4096;
+  return batch * m * 16 + 4096;
 }
 
 int xft_mehler(const void* in, void* out, int64_t batch, int64_t n, const double* z, int64_t z_stride,

@@ -46,7 +46,10 @@ int run_large_chirpz(int lct, int bare, const void* in, void* out, int64_t batch
                      const void* hspec, int64_t m, cudaStream_t st);
 struct OpMehlerRow;
 int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm, int l,
-                     int64_t n, cudaStream_t st, void* scratch = nullptr);
+                     int64_t n, cudaStream_t st, void* scratch, const void* hspec);
+// plan time: the permuted kernel spectra of a four-step Mehler class ([rows][2^l] double2)
+int large_mehler_spectrum(long long rows, const int* rowlist, const OpMehlerRow* prm, int l, void* hs_out,
+                          cudaStream_t st);
 
 // column LCT of a [R][ncols] slab with row stride ld (xft_large.cu); abcd on the host.
 // ws: scratch of R*ld elements when R > 1024.

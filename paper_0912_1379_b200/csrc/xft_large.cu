@@ -712,8 +712,9 @@ int large_chirpz(int lct, int bare, const C* in, C* out, int64_t batch, int64_t 
 }
 
 // Mehler rows whose window needs M > in-CTA limit (complex128)
-int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm,
-                     int l, int64_t n, cudaStream_t st, void* scratch) {
+// plan time: the permuted kernel spectra of a four-step Mehler class, [rows][M] into hs
+int large_mehler_spectrum(long long rows, const int* rowlist, const OpMehlerRow* prm, int l, void* hs_out,
+                          cudaStream_t st) {
   using C = double2;
   constexpr int W = tile_w<C>();
   const Shape sh = split(l);
@@ -721,30 +722,42 @@ int run_large_mehler(const void* in, void* out, long long rows, const int* rowli
   const void* twm = nullptr;
   int rc = natural_twiddles(sh.M, XFT_C128, &twm);
   if (rc) return rc;
-  DevBuf<C> hs(st), us(st);  // caller scratch (2 rows x M per row) when given, else stream-ordered
+  C* hs = static_cast<C*>(hs_out);
+  const long long t1 = rows * (M2 / W), t2 = rows * (M1 / W);
+  OpColsMehlerH h1{{GenMehlerH{prm, rowlist, sh.M}, hs, static_cast<const C*>(twm), M2, W, sh.M, 0}};
+  if ((rc = tile<C, true, true, -1>(sh.l1, t1, h1, st))) return rc;
+  OpRowsPerm<C> h2{hs, M1, M2, W, sh.M};
+  return tile<C, false, false, -1>(sh.l2, t2, h2, st);
+}
+
+// data passes of a four-step Mehler class with the plan's spectra hspec ([rows][M], permuted)
+int run_large_mehler(const void* in, void* out, long long rows, const int* rowlist, const OpMehlerRow* prm,
+                     int l, int64_t n, cudaStream_t st, void* scratch, const void* hspec) {
+  using C = double2;
+  constexpr int W = tile_w<C>();
+  const Shape sh = split(l);
+  const int M1 = 1 << sh.l1, M2 = 1 << sh.l2;
+  const void* twm = nullptr;
+  int rc = natural_twiddles(sh.M, XFT_C128, &twm);
+  if (rc) return rc;
+  DevBuf<C> us(st);  // caller scratch (one row x M per row) when given, else stream-ordered
   if (scratch) {
-    hs.p = static_cast<C*>(scratch);
-    us.p = hs.p + (size_t)rows * sh.M;
-    hs.st = us.st = nullptr;
-  } else if ((rc = hs.alloc((size_t)rows * sh.M)) || (rc = us.alloc((size_t)rows * sh.M))) {
+    us.p = static_cast<C*>(scratch);
+    us.st = nullptr;
+  } else if ((rc = us.alloc((size_t)rows * sh.M))) {
     return rc;
   }
   struct Release {  // caller scratch is not freed
-    DevBuf<C>& a; DevBuf<C>& b; bool own;
-    ~Release() { if (!own) { a.p = nullptr; b.p = nullptr; } }
-  } release{hs, us, scratch == nullptr};
+    DevBuf<C>& a; bool own;
+    ~Release() { if (!own) a.p = nullptr; }
+  } release{us, scratch == nullptr};
   const long long t1 = rows * (M2 / W), t2 = rows * (M1 / W);
   const double half = host_half_step(n);
-  // kernel spectrum, permuted
-  OpColsMehlerH h1{{GenMehlerH{prm, rowlist, sh.M}, hs.p, static_cast<const C*>(twm), M2, W, sh.M, 0}};
-  if ((rc = tile<C, true, true, -1>(sh.l1, t1, h1, st))) return rc;
-  OpRowsPerm<C> h2{hs.p, M1, M2, W, sh.M};
-  if ((rc = tile<C, false, false, -1>(sh.l2, t2, h2, st))) return rc;
   // data: columns, rows (forward x H inverse), inverse columns with the output weights
   OpColsMehlerU u1{{GenMehlerU{static_cast<const C*>(in), prm, rowlist, half, n}, us.p,
                     static_cast<const C*>(twm), M2, W, sh.M, 0}};
   if ((rc = tile<C, true, true, -1>(sh.l1, t1, u1, st))) return rc;
-  OpRowsConv<C> u2{us.p, hs.p, sh.M, static_cast<const C*>(twm), M1, M2, W, sh.M};
+  OpRowsConv<C> u2{us.p, static_cast<const C*>(hspec), sh.M, static_cast<const C*>(twm), M1, M2, W, sh.M};
   if ((rc = tile<C, false, false, -1>(sh.l2, t2, u2, st))) return rc;
   OpColsInvMehler u3{{us.p, PostMehler{static_cast<C*>(out), prm, rowlist, half, n}, M2, W, sh.M}};
   if ((rc = tile<C, true, true, +1>(sh.l1, t1, u3, st))) return rc;
@@ -1048,6 +1061,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void clu_st(uint32_t a, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void clu_st(uint32_t a, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+#ifndef XFT_CLU_PUSH
+#define XFT_CLU_PUSH 1  // cross-CTA exchange by remote stores into the owner's buffer (0: remote loads)
+#endif
+
 __device__ __forceinline__ void clu_sync_relaxed() {  // WAR only: the peers' DSMEM loads have been consumed
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
@@ -1068,12 +1091,18 @@ struct CluCfg {
   // consecutive positions; LS = S/W (mod S) puts them in S distinct slots
   static constexpr int S = 128 / (int)sizeof(C);
   static constexpr int LS = Fft::NP + (((S / W) - Fft::NP % S) % S + S) % S;
-  static constexpr int BUF = ((W * LS > L * W ? W * LS : L * W) * (int)sizeof(C) + 127) / 128 * 128 / (int)sizeof(C);
+  static constexpr int GS = K * W + 8;  // (see PAIRS below)
+  static constexpr int BUF0 = W * LS > L * W ? W * LS : L * W;
+  static constexpr int BUF1 = XFT_CLU_PUSH && (L / K) * GS > BUF0 ? (L / K) * GS : BUF0;
+  static constexpr int BUF = (BUF1 * (int)sizeof(C) + 127) / 128 * 128 / (int)sizeof(C);
   static constexpr size_t SMEM = NBUF * size_t(BUF) * sizeof(C);
   static constexpr int BOXM = L < 256 ? L : 256;
   static constexpr int EW = (int)sizeof(C) / 8;  // 8-byte tensor elements per sample
   static constexpr int PAIRS = (L / K) * W;      // (k1, column) pairs a CTA finishes per group
+  // push layout of the gathered values in the owner's buffer: [k1 local][source CTA][column],
+  // row stride GS = K W + 8 (4 k1 rows of a warp fall on the two halves of the banks)
   static_assert(THREADS <= 1024 && L % K == 0 && W <= S, "cluster column shape");
+  static_assert(!XFT_CLU_PUSH || (L / K) * GS <= BUF, "push layout fits the group buffer");
 };
 
 template <class Cfg>
@@ -1134,29 +1163,56 @@ xft_colclu_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __re
       }
     }
     pipe_passes<typename Cfg::Fft, 0>(v, X + w * Cfg::LS, j, tw, noop);
-    __syncthreads();  // the exchange buffer is dead; it now receives Y[k1][w]
-#pragma unroll
-    for (int s = 0; s < E; ++s) {
-      const int k1 = j + s * TR;
-      C y = v[s];
-      if constexpr (sizeof(C) == 8) {  // w_R^{c k1}, exact turns
-        y = cmul(walk_phasor((0u - ((uint32_t)(c * k1) << (32 - LOGR))) + ((512u - 326u) << 0)), y);
-      } else {
-        double sn, cs;
-        sincospi(-2.0 * (double)(c * k1) / (double)(K * L), &sn, &cs);
-        y = cmul(make_double2(cs, sn), y);
-      }
-      X[k1 * W + w] = y;
-    }
-    clu_sync();
     const uint32_t xaddr = smem_addr(X);
+    if constexpr (XFT_CLU_PUSH) {
+      // every CTA of the cluster is done with its buffer: Y_c[k1][w] goes straight into the
+      // buffer of the CTA that owns k1 (remote stores: no load latency on the critical path)
+      clu_sync();
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        const int k1 = j + s * TR;
+        C y = v[s];
+        if constexpr (sizeof(C) == 8) {  // w_R^{c k1}, exact turns
+          y = cmul(walk_phasor((0u - ((uint32_t)(c * k1) << (32 - LOGR))) + ((512u - 326u) << 0)), y);
+        } else {
+          double sn, cs;
+          sincospi(-2.0 * (double)(c * k1) / (double)(K * L), &sn, &cs);
+          y = cmul(make_double2(cs, sn), y);
+        }
+        const int owner = k1 / (L / K), kl = k1 % (L / K);
+        clu_st(clu_map(xaddr + (uint32_t)((kl * Cfg::GS + c * W + w) * sizeof(C)), owner), y);
+      }
+      clu_sync();  // every push into this CTA's buffer has landed
+    } else {
+      __syncthreads();  // the exchange buffer is dead; it now receives Y[k1][w]
+#pragma unroll
+      for (int s = 0; s < E; ++s) {
+        const int k1 = j + s * TR;
+        C y = v[s];
+        if constexpr (sizeof(C) == 8) {  // w_R^{c k1}, exact turns
+          y = cmul(walk_phasor((0u - ((uint32_t)(c * k1) << (32 - LOGR))) + ((512u - 326u) << 0)), y);
+        } else {
+          double sn, cs;
+          sincospi(-2.0 * (double)(c * k1) / (double)(K * L), &sn, &cs);
+          y = cmul(make_double2(cs, sn), y);
+        }
+        X[k1 * W + w] = y;
+      }
+      clu_sync();
+    }
 #pragma unroll 1
     for (int p = t; p < Cfg::PAIRS; p += T) {
       const int pw = p % W, k1 = c * (L / K) + p / W;
       C y[K];
-      const uint32_t la = xaddr + (uint32_t)((k1 * W + pw) * sizeof(C));
+      if constexpr (XFT_CLU_PUSH) {
+        const C* g = X + (p / W) * Cfg::GS + pw;
 #pragma unroll
-      for (int cc = 0; cc < K; ++cc) clu_ld(clu_map(la, cc), y[cc]);
+        for (int cc = 0; cc < K; ++cc) y[cc] = g[cc * W];
+      } else {
+        const uint32_t la = xaddr + (uint32_t)((k1 * W + pw) * sizeof(C));
+#pragma unroll
+        for (int cc = 0; cc < K; ++cc) clu_ld(clu_map(la, cc), y[cc]);
+      }
       dft_r<K, -1>(y);
       C* dst = out + (long long)k1 * ld + (long long)g * W + pw;
       const long long step = (long long)L * ld;
@@ -1173,7 +1229,11 @@ xft_colclu_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __re
         for (int k2 = 0; k2 < K; ++k2) dst[k2 * step] = ColPhase<C>::post(ck, cptab, k1 + (long long)L * k2, y[k2]);
       }
     }
-    clu_sync_relaxed();  // every peer is done reading this CTA's Y
+    if constexpr (XFT_CLU_PUSH) {
+      __syncthreads();  // this CTA's own reads of its buffer are done (peers push only after the next A')
+    } else {
+      clu_sync_relaxed();  // every peer is done reading this CTA's Y
+    }
     if (t == 0) {
       const int gn = g + NB * nq;
       if (gn < ngroups) issue(gn, b);
