@@ -1068,7 +1068,7 @@ __device__ __forceinline__ void clu_st(uint32_t a, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
 #ifndef XFT_CLU_PUSH
-#define XFT_CLU_PUSH 1  // cross-CTA exchange by remote stores into the owner's buffer (0: remote loads)
+#define XFT_CLU_PUSH 0  // 1: cross-CTA exchange by remote stores into the owner's buffer (A/B cfg5: 3.09 vs 2.81 ms: off)
 #endif
 
 __device__ __forceinline__ void clu_sync_relaxed() {  // WAR only: the peers' DSMEM loads have been consumed

@@ -30,11 +30,12 @@ with torch.cuda.stream(s):
 g.replay()
 torch.cuda.synchronize()
 best = 1e9
-for _ in range(3):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    g.replay()
-    e1.record(s)
-    torch.cuda.synchronize()
-    best = min(best, e0.elapsed_time(e1) / reps)
+with torch.cuda.stream(s):  # replay on the stream the events are recorded on
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        g.replay()
+        e1.record(s)
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / reps)
 print(f"{tag}: cfg3 {best:.4f} ms per step")
