@@ -1017,6 +1017,9 @@ int lct_cols_narrow(const void* in, void* out, void* ws, int64_t R, int64_t ncol
 #ifndef XFT_CLU_NB
 #define XFT_CLU_NB 1  // group buffers per CTA (2: double-buffered TMA)
 #endif
+#ifndef XFT_CLU_W64
+#define XFT_CLU_W64 8  // c64 columns per cluster group (8: 64-byte row segments)
+#endif
 #ifndef XFT_CLU_MINB
 #define XFT_CLU_MINB 2  // resident CTAs per SM the registers are sized for
 #endif
@@ -1319,7 +1322,7 @@ template <class C>
 int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
                      const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1,
                      bool probe = false) {
-  constexpr int W = sizeof(C) == 8 ? 8 : 4;
+  constexpr int W = sizeof(C) == 8 ? XFT_CLU_W64 : 4;
   if (!XFT_COLCLU || ncols % W) return XFT_ENOTSUP;
   switch (log2_of(R)) {
 #if XFT_CLU14 == 1

@@ -214,7 +214,8 @@ __device__ __forceinline__ void make_coef(Coef64& c, const double* p, const Abcd
 #define XFT_WALK_MIN_LOG2N 11  // c128 rows shorter than 2^11 use the per-element table path (accuracy)
 #endif
 #ifndef XFT_WALK_SMOOTH_BELOW
-#define XFT_WALK_SMOOTH_BELOW 2048.0  // rows with max |phase| below this skip the rounding corrections
+#define XFT_WALK_SMOOTH_BELOW 8192.0  // rows with max |phase| below this skip the rounding corrections (max row
+                                      // error 4.4e-13 in [4096, 8192) vs 1.2e-13 corrected; c128 119.3 -> 116.9 us)
 #endif
 struct DD {
   double hi, lo;

@@ -147,10 +147,13 @@ def test_config2_full_batch(torch, X, dtype, tol):
 @pytest.mark.parametrize("n", [64, 1024, 4096, 8192])
 def test_c128_chirp_modes(torch, X, n):
     """c128 rows whose largest chirp phase puts each side in every evaluation mode:
-    smooth walk (< 2^11 rad), walk + per-element rounding correction (< 2^24),
-    table (< 1e12), pre-reduced table (beyond), and a = 0 / d = 0 rows."""
+    smooth walk (< 2^13 rad, incl. rows just below the threshold), walk + per-element
+    rounding correction (< 2^24), table (< 1e12), pre-reduced table (beyond), and
+    a = 0 / d = 0 rows."""
     rows = []
-    for al in (math.pi / 2, 1.3, 0.3, 3.02e-4, math.pi - 6.56e-4, 1e-6, 1e-10):
+    xm2 = ((n - 1) * math.pi / math.sqrt(2 * n) / 2) ** 2  # largest x^2 on the grid
+    edge = [math.atan(0.5 * xm2 / p) for p in (8150.0, 8250.0)]  # max |phase| just below / above 2^13
+    for al in (math.pi / 2, 1.3, 0.3, 3.02e-4, math.pi - 6.56e-4, 1e-6, 1e-10, *edge):
         rows.append((math.cos(al), math.sin(al), -math.sin(al), math.cos(al)))
     for a, b, d in ((2.0, 1.0, 2000.0), (0.5, 1.0, 1e6), (3.0, 1.0, 1e10), (1e8, 1.0, 0.0), (0.0, 1.0, 1e7),
                     (-2.5, -0.7, 33.0)):
