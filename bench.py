@@ -456,8 +456,9 @@ def measure_config(name, args, rank, world, local_rank, steps, replicate=False, 
         kern_runs = [runner(k) for k in range(len(work))] if len(work) > 1 else [step_run]
         step_run(max(args.warmup, 3))  # warm-up (graphs for the remainder are captured here too)
         torch.cuda.synchronize()
-        kern_ms = [max_over_ranks(timed(kern_runs[k], steps)) / steps for k in range(len(work))] \
-            if len(work) > 1 else None
+        # each item alone (the roofline's per-kernel time): median of 3 timed runs of `steps` launches
+        kern_ms = [statistics.median(max_over_ranks(timed(kern_runs[k], steps)) / steps for _ in range(3))
+                   for k in range(len(work))] if len(work) > 1 else None
         if clocks:
             with ClockSampler(local_rank) as clk:
                 total_ms = timed(step_run, steps)
@@ -593,8 +594,8 @@ def roofline_of(name, rec, world, peak, peak_src, fp64_peak):
     roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
             "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"{kname} {dom}",
             "peak_source": peak_src,
-            "measured": "each item alone: K graph-replayed launches on its stream, CUDA events; "
-                        "step_achieved = all items' algorithmic bytes / step time",
+            "measured": "each item alone: K graph-replayed launches on its stream, CUDA events, median of 3 "
+                        "runs; step_achieved = all items' algorithmic bytes / step time",
             "step_achieved": bytes_of(work) / (rec["ms_per_step"] * 1e-3) / 1e9}
     if "fp64" in per[dom]:
         roof["fp64"] = per[dom]["fp64"]

@@ -15,7 +15,7 @@ from paper_0912_1379_b200 import ops  # noqa: E402
 n = 16384
 sets = [torch.randn(n, n, dtype=torch.complex64, device="cuda") for _ in range(2)]
 outs = [torch.empty_like(v) for v in sets]
-p = (1.0, 0.25, 0.0, 1.0)
+p = torch.tensor([1.0, 0.25, 0.0, 1.0], dtype=torch.float64, device="cuda")  # device params: capturable
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     for v, o in zip(sets, outs):
