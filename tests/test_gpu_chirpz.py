@@ -253,3 +253,27 @@ def test_mehler_config3_every_row_against_dense_gpu_oracle(torch, X):
             e = rel_l2(got[s + r], ref[r])
             worst.append(e / _mehler_tol(z[s + r]))
     assert max(worst) <= 1.0, (int(np.argmax(worst)), max(worst))
+
+
+def test_mehler_caller_workspace_matches_internal_scratch(torch, X):
+    """xft_mehler with a caller workspace (xft_mehler_workspace_bytes; the classes run one after
+    another on the caller's stream) == the default path (internal side streams and scratch)."""
+    import ctypes
+
+    from paper_0912_1379_b200 import _native, ops
+    from paper_0912_1379_b200 import workloads
+
+    c3 = workloads.config3(rows=48)
+    z = c3.extra["z"]
+    v = dev(torch, c3.values)
+    ref = X.mehler_rows(v, z)
+    n = v.shape[1]
+    nbytes = int(_native.lib().xft_mehler_workspace_bytes(v.shape[0], n))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=v.device)
+    out = torch.empty_like(v)
+    zh = np.ascontiguousarray(np.stack([z.real, z.imag], axis=1))
+    _native.call("xft_mehler", v.data_ptr(), out.data_ptr(), v.shape[0], n, zh.ctypes.data, 2, ws.data_ptr(),
+                 ops._stream_ptr(v.device))
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    del ctypes
