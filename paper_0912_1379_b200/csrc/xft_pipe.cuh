@@ -492,6 +492,9 @@ struct PipeCfg {
   static constexpr int MINB = MINB_;
 };
 
+#ifndef XFT_DFT_COLTW
+#define XFT_DFT_COLTW 1  // c128 plain-DFT radix-16 passes: exact twiddles applied per 4-point column
+#endif
 #ifndef XFT_PDL
 #define XFT_PDL 0  // 1: row kernels launched with programmatic stream serialization (A/B: c128 119.05 vs 119.3 us, c64 53.6 vs 52.6 us: off)
 #endif
@@ -525,6 +528,9 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
   // c128 LCT-mode radix-16 passes: twiddles fused into the butterfly's first stage
   constexpr bool FUSED = (Cfg::C128 ? XFT_FUSE_TW : XFT_FUSE_TW64) && R == 16 && XFT_DFT16_44 && NS > 1 &&
                          XFT_SKELETON == 0 && !XFT_NOTW && XFT_TWGEN && (!Cfg::C128 || Cfg::MODE != MODE_DFT);
+  // exact-table twiddles column by column (the passes that do not generate them: c128 plain DFT)
+  constexpr bool COLTW = !FUSED && XFT_DFT_COLTW && R == 16 && XFT_DFT16_44 && NS > 1 && XFT_SKELETON == 0 &&
+                         !XFT_NOTW && !XFT_TWPRE && Cfg::C128 && Cfg::MODE == MODE_DFT;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int i = j + b * TR;
@@ -586,6 +592,23 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
           for (int r = 1; r < 8; ++r) u[8 * b + r] = cmul(u[8 * b + r], cmul(h, lo[r]));
         }
       }
+    } else if constexpr (COLTW) {
+      // exact table twiddles (plain-DFT passes: chirp-z / Mehler convolutions), applied one
+      // 4-point column of the 4 x 4 butterfly at a time, the column's 4-point DFT right after:
+      // at most 3 twiddles are live (c128 M = 8192 Mehler rows: spills 868 -> see ptxas log)
+      const C* twp = tw + Cfg::twoff(P) + k;
+#pragma unroll
+      for (int n2 = 0; n2 < 4; ++n2) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int t = 4 * q + n2;
+          if (t == 0) continue;
+          C w = __ldg(twp + (t - 1) * NS);
+          if (Cfg::SIGN > 0) w = cconj(w);
+          u[t] = cmul(u[t], w);
+        }
+        dft4<Cfg::SIGN>(u[n2], u[4 + n2], u[8 + n2], u[12 + n2]);
+      }
     } else if constexpr (NS > 1 && XFT_SKELETON == 0 && !XFT_NOTW) {
       const C* twp = tw + Cfg::twoff(P) + k;
 #pragma unroll
@@ -597,7 +620,7 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
         u[t] = cmul(u[t], w);
       }
     }
-    if constexpr (FUSED) dft16_44_rows<Cfg::SIGN>(u);  // first stage done above
+    if constexpr (FUSED || COLTW) dft16_44_rows<Cfg::SIGN>(u);  // first stage done above
     else if constexpr (XFT_SKELETON == 0) dft_r<R, Cfg::SIGN>(u);
 #pragma unroll
     for (int t = 0; t < R; ++t) v[b + t * NB] = u[t];

@@ -42,8 +42,12 @@ int get_tables(int64_t n, int dtype, Tables* out, int radix = -1);
 #ifndef XFT_BLUE_E13
 #define XFT_BLUE_E13 16  // radix of the c128 M = 8192 chirp-z / Mehler CTA (32: 256 threads)
 #endif
+#ifndef XFT_BLUE_E12
+#define XFT_BLUE_E12 8  // radix of the c128 M = 4096 chirp-z / Mehler CTA (8: 512 threads, no spills; cfg3 0.344 -> 0.338 ms)
+#endif
 constexpr int blue_radix(int dtype, int l) {
   return (dtype == 1 && l == 13) ? XFT_BLUE_E13
+         : (dtype == 1 && l == 12) ? XFT_BLUE_E12
          : pipe_radix(dtype, l) < (1 << (l - 1)) ? pipe_radix(dtype, l) : (1 << (l - 1));
 }
 
