@@ -94,9 +94,13 @@ def _clock_worker(index, period, stop, out):
 
 
 class ClockSampler:
-    def __init__(self, index: int, period_s: float = 0.005):
-        self.index, self.period = index, period_s
-        self.samples, self.reasons, self.max_mhz, self.ok = [], 0, None, False
+    """NVML SM clocks and throttle reasons sampled by a child process every `period_s` during the
+    timed region.  A short region (the driver's 20-step runs last ~3 ms) may see no sample at all:
+    the summary then uses the samples nearest to it (within `window_s`) and says so."""
+
+    def __init__(self, index: int, period_s: float = 0.0005, window_s: float = 0.05):
+        self.index, self.period, self.window = index, period_s, window_s
+        self.samples, self.reasons, self.max_mhz, self.ok, self.where = [], 0, None, False, "inside"
 
     def __enter__(self):
         import multiprocessing as mp
@@ -120,6 +124,9 @@ class ClockSampler:
         if res is not None:
             rows, self.max_mhz = res
             inside = [r for r in rows if self._t0 <= r[0] <= t1]  # the timed region only
+            if not inside:  # region shorter than the sampling period: the nearest samples
+                inside = [r for r in rows if self._t0 - self.window <= r[0] <= t1 + self.window]
+                self.where = f"nearest (within {self.window * 1e3:.0f} ms of a {1e3 * (t1 - self._t0):.1f} ms region)"
             self.samples = [r[1] for r in inside]
             for r in inside:
                 self.reasons |= r[2]
@@ -130,7 +137,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
         names = [v for k, v in _REASONS.items() if self.reasons & k and v != "gpu_idle"]
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples), "window": self.where}
 
 
 # ---------------------------------------------------------------------------

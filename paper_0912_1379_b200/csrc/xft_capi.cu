@@ -187,7 +187,7 @@ int launch_pipe(const LaunchArgs& a) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = XFT_PDL ? 1 : 0;
+  cfg.numAttrs = (sizeof(C) == 16 ? XFT_PDL_C128 : XFT_PDL_C64) ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<const C*>(a.in), static_cast<C*>(a.out), a.batch,
                                            a.abcd, (long long)a.stride, a.uni, static_cast<const C*>(a.tb.tw),
                                            static_cast<const C*>(a.tb.ptab), a.tb.gtab, a.tb.cn, kc, a.seg_log2w,

@@ -495,9 +495,13 @@ struct PipeCfg {
 #ifndef XFT_DFT_COLTW
 #define XFT_DFT_COLTW 1  // c128 plain-DFT radix-16 passes: exact twiddles applied per 4-point column
 #endif
-#ifndef XFT_PDL
-#define XFT_PDL 0  // 1: row kernels launched with programmatic stream serialization (A/B: c128 119.05 vs 119.3 us, c64 53.6 vs 52.6 us: off)
+#ifndef XFT_PDL_C128
+#define XFT_PDL_C128 1  // c128 row kernels launched with programmatic stream serialization (griddepcontrol)
 #endif
+#ifndef XFT_PDL_C64
+#define XFT_PDL_C64 0   // c64: A/B 53.6 vs 52.6 us with it: off
+#endif
+#define XFT_PDL (XFT_PDL_C128 || XFT_PDL_C64)
 __device__ __forceinline__ void griddep_launch_dependents() {
   if (XFT_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
