@@ -98,7 +98,7 @@ class ClockSampler:
     timed region.  A short region (the driver's 20-step runs last ~3 ms) may see no sample at all:
     the summary then uses the samples nearest to it (within `window_s`) and says so."""
 
-    def __init__(self, index: int, period_s: float = 0.002, window_s: float = 0.05):
+    def __init__(self, index: int, period_s: float = 0.002, window_s: float = 0.25):
         self.index, self.period, self.window = index, period_s, window_s
         self.samples, self.reasons, self.max_mhz, self.ok, self.where = [], 0, None, False, "inside"
 
@@ -109,7 +109,7 @@ class ClockSampler:
         self._stop, self._q = ctx.Event(), ctx.Queue()
         self._p = ctx.Process(target=_clock_worker, args=(self.index, self.period, self._stop, self._q), daemon=True)
         self._p.start()
-        time.sleep(0.05)  # the child is sampling before the timed region starts
+        time.sleep(0.25)  # the child is sampling before the timed region starts
         self._t0 = time.perf_counter()
         return self
 
