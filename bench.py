@@ -101,6 +101,7 @@ class ClockSampler:
     def __init__(self, index: int, period_s: float = 0.002, window_s: float = 0.25):
         self.index, self.period, self.window = index, period_s, window_s
         self.samples, self.reasons, self.max_mhz, self.ok, self.where = [], 0, None, False, "inside"
+        self.probed = []
 
     def __enter__(self):
         import multiprocessing as mp
@@ -124,6 +125,7 @@ class ClockSampler:
         if res is not None:
             rows, self.max_mhz = res
             inside = [r for r in rows if self._t0 <= r[0] <= t1]  # the timed region only
+            inside += [(t1, c, why) for c, why in self.probed]  # taken while the timed work ran
             if not inside:  # region shorter than the sampling period: the nearest samples
                 inside = [r for r in rows if self._t0 - self.window <= r[0] <= t1 + self.window]
                 self.where = f"nearest (within {self.window * 1e3:.0f} ms of a {1e3 * (t1 - self._t0):.1f} ms region)"
@@ -131,6 +133,20 @@ class ClockSampler:
             for r in inside:
                 self.reasons |= r[2]
             self.ok = True
+
+    def probe(self, count=2):
+        """In-process samples taken while the timed work is still running on the GPU (the graph
+        launches return immediately; called between the end event and the synchronize)."""
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            for _ in range(count):
+                self.probed.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                    pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        except Exception:
+            pass
 
     def summary(self):
         if not self.ok:
@@ -439,7 +455,7 @@ def measure_config(name, args, rank, world, local_rank, steps, replicate=False, 
         if world > 1:
             torch.distributed.barrier()
 
-    def timed(run, n):
+    def timed(run, n, during=None):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         barrier()
@@ -447,6 +463,8 @@ def measure_config(name, args, rank, world, local_rank, steps, replicate=False, 
         e0.record(stream)
         run(n)
         e1.record(stream)
+        if during is not None:  # host-side work while the GPU is still executing the timed steps
+            during()
         torch.cuda.synchronize()
         barrier()
         return e0.elapsed_time(e1)
@@ -468,7 +486,7 @@ def measure_config(name, args, rank, world, local_rank, steps, replicate=False, 
                    for k in range(len(work))] if len(work) > 1 else None
         if clocks:
             with ClockSampler(local_rank) as clk:
-                total_ms = timed(step_run, steps)
+                total_ms = timed(step_run, steps, during=clk.probe)
         else:
             clk = None
             total_ms = timed(step_run, steps)
