@@ -485,8 +485,8 @@ def measure_config(name, args, rank, world, local_rank, steps, replicate=False, 
         kern_ms = [statistics.median(max_over_ranks(timed(kern_runs[k], steps)) / steps for _ in range(3))
                    for k in range(len(work))] if len(work) > 1 else None
         if clocks:
-            with ClockSampler(local_rank) as clk:
-                total_ms = timed(step_run, steps, during=clk.probe)
+            with ClockSampler(local_rank, period_s=args.clock_period) as clk:
+                total_ms = timed(step_run, steps, during=clk.probe if args.clock_probe else None)
         else:
             clk = None
             total_ms = timed(step_run, steps)
@@ -713,6 +713,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--extra-steps", type=int, default=200, help="steps for the per-config extras")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--clock-period", type=float, default=0.002, help="NVML clock sampling period (s)")
+    ap.add_argument("--clock-probe", type=int, default=1, help="1: in-process clock probes while the steps run")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: the step's independent batches (c64, c128) on their own streams inside the graph")

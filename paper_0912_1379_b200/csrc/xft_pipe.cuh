@@ -496,7 +496,9 @@ struct PipeCfg {
 #define XFT_DFT_COLTW 1  // c128 plain-DFT radix-16 passes: exact twiddles applied per 4-point column
 #endif
 #ifndef XFT_PDL_C128
-#define XFT_PDL_C128 1  // c128 row kernels launched with programmatic stream serialization (griddepcontrol)
+#define XFT_PDL_C128 0  // 1: c128 row kernels launched with programmatic stream serialization (griddepcontrol):
+                        // no gain alone (116.6 vs 116.7 us), and the early CTAs hold SM slots the concurrent
+                        // c64 batch of a config-2 step needs (step 0.159 -> 0.170 ms): off
 #endif
 #ifndef XFT_PDL_C64
 #define XFT_PDL_C64 0   // c64: A/B 53.6 vs 52.6 us with it: off
