@@ -1244,6 +1244,125 @@ xft_colclu_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __re
   }
 }
 
+// ---------------------------------------------------------------------------
+// K6b: the same cluster column transform with the cross-CTA exchange done by the
+// copy engines.  Per group: TMA the column group into one of two buffers (the
+// next group's load is issued while this one is exchanged), FFT, write
+// Y_c[k1][w] k1-major, then ONE thread issues K bulk copies
+// (cp.async.bulk.shared::cluster.shared::cta, 4 KB each) that deliver the k1
+// slice owned by CTA o straight into o's receive buffer, completing on o's
+// mbarrier; each CTA waits only on its own mbarrier (no cluster-wide barrier
+// on the data path) and gathers locally.  The only cluster barrier is split:
+// arrive after this CTA's gather, wait one group later before the next copies
+// (the receive buffers are free) -- the FFT of the next group sits in between.
+// One CTA per SM (two group buffers + the receive buffer: ~200 KB).
+// ---------------------------------------------------------------------------
+#ifndef XFT_CLU_BULK
+#define XFT_CLU_BULK 1  // c64 16-CTA column clusters with the copy-engine exchange (K6b)
+#endif
+__device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint32_t mbar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ void clu_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void clu_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+xft_colclu2_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __restrict__ out, long long ld,
+                   int ngroups, ColChirp ck, const double2* __restrict__ ptab, const double2* __restrict__ cptab,
+                   const typename Cfg::C* __restrict__ tw) {
+  using C = typename Cfg::C;
+  static_assert(sizeof(C) == 8, "K6b is the c64 path");
+  constexpr int K = Cfg::K, L = Cfg::L, W = Cfg::W, E = Cfg::E, TR = Cfg::TR, T = Cfg::THREADS;
+  constexpr int LOGR = Cfg::LOGL + ilog2(K);
+  constexpr int SL = (L / K) * W;  // elements of one k1 slice (the chunk one CTA sends another)
+  extern __shared__ __align__(128) unsigned char xft_smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t rxbar;
+  C* const buf0 = reinterpret_cast<C*>(xft_smem);
+  C* const RX = buf0 + 2 * Cfg::BUF;  // [source CTA][k1 local][column]
+  const int c = (int)clu_rank();
+  const int q = (int)clu_id(), nq = (int)clu_count();
+  const int t = threadIdx.x, w = t % W, j = t / W;
+  auto noop = []() {};
+  auto issue = [&](int g, int b) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[b], (uint32_t)(L * W * sizeof(C)));
+#pragma unroll 1
+    for (int m0 = 0; m0 < L; m0 += Cfg::BOXM)
+      tma_load_3d(buf0 + b * Cfg::BUF + m0 * W, &map, g * W * Cfg::EW, c, m0, &bars[b]);
+  };
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&rxbar, 1);
+    fence_mbar_init();
+  }
+  clu_sync();  // every peer's receive mbarrier is initialised before any copy completes on it
+  if (t == 0 && q < ngroups) issue(q, 0);
+  const uint32_t rx_local = smem_addr(RX + c * SL), rxbar_local = smem_addr(&rxbar);
+  int it = 0;
+  for (int g = q; g < ngroups; g += nq, ++it) {
+    const int b = it & 1;
+    C* const X = buf0 + b * Cfg::BUF;
+    mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
+    C v[E];
+    {
+      // this thread's rows r = r0 + s K TR: the chirp + boundary phase is a quadratic walk in s
+      const int r0 = c + K * j;
+      const uint32_t bt0 = ((uint32_t)(r0 & 1) << 31) - ((uint32_t)r0 << (31 - LOGR));
+      TurnWalk wk(ck.dq_in, 2 * r0 - (1 << LOGR) + 1, 2 * K * TR, (unsigned long long)bt0 << 32,
+                  (unsigned long long)(K * TR) << (63 - LOGR));
+#pragma unroll
+      for (int s = 0; s < E; ++s) v[s] = cmul(walk_phasor(wk.next()), X[(j + s * TR) * W + w]);
+    }
+    pipe_passes<typename Cfg::Fft, 0>(v, X + w * Cfg::LS, j, tw, noop);
+    __syncthreads();  // the exchange buffer is dead; it now holds Y[k1][w], k1-major
+#pragma unroll
+    for (int s = 0; s < E; ++s) {
+      const int k1 = j + s * TR;
+      X[k1 * W + w] = cmul(walk_phasor((0u - ((uint32_t)(c * k1) << (32 - LOGR))) + ((512u - 326u) << 0)), v[s]);
+    }
+    fence_proxy_async_smem();  // the copy engine reads what these threads wrote
+    if (it > 0) clu_wait();    // every CTA has gathered the previous group: receive buffers are free
+    __syncthreads();
+    if (t == 0) {
+      // the other buffer held the previous group's Y, whose copies have all landed (the wait above)
+      const int gn = g + nq;
+      if (gn < ngroups) issue(gn, b ^ 1);
+      mbar_arrive_expect_tx(&rxbar, (uint32_t)(L * W * sizeof(C)));  // K chunks of this group
+      const uint32_t src0 = smem_addr(X);
+#pragma unroll 1
+      for (int o = 0; o < K; ++o)
+        bulk_s2c(clu_map(rx_local, o), src0 + (uint32_t)(o * SL * sizeof(C)), (uint32_t)(SL * sizeof(C)),
+                 clu_map(rxbar_local, o));
+    }
+    mbar_wait(&rxbar, (uint32_t)(it & 1));
+#pragma unroll 1
+    for (int p = t; p < Cfg::PAIRS; p += T) {
+      const int pw = p % W, kl = p / W, k1 = c * (L / K) + kl;
+      C y[K];
+#pragma unroll
+      for (int cc = 0; cc < K; ++cc) y[cc] = RX[cc * SL + kl * W + pw];
+      dft_r<K, -1>(y);
+      C* dst = out + (long long)k1 * ld + (long long)g * W + pw;
+      const long long step = (long long)L * ld;
+      // output rows k1 + L k2: post-chirp + boundary + arg G walk in k2
+      const uint32_t bt0 = ((uint32_t)(k1 & 1) << 31) - ((uint32_t)k1 << (31 - LOGR)) + ck.gq;
+      TurnWalk wk(ck.dq_out, 2 * k1 - (1 << LOGR) + 1, 2 * L, (unsigned long long)bt0 << 32,
+                  (unsigned long long)L << (63 - LOGR));
+      const float2 gg = make_float2(ck.gabs, ck.gabs);
+#pragma unroll
+      for (int k2 = 0; k2 < K; ++k2) dst[k2 * step] = cmul(walk_phasor(wk.next()), p_mul(y[k2], gg));
+    }
+    clu_arrive();  // this CTA's receive buffer may be refilled
+  }
+  if (it > 0) clu_wait();  // pairs the last arrive; no peer touches this CTA's memory afterwards
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -1258,7 +1377,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_encoder() {
 }
 
 
-template <class C, int K, int LOGL, int W, int NBUF = 1, int MINB = 2>
+template <class C, int K, int LOGL, int W, int NBUF = 1, int MINB = 2, bool BULK = false>
 int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, const ColChirp& ck,
                   const double2* ptab, const double2* cptab, cudaStream_t st, int64_t ld_out = -1,
                   bool probe = false) {
@@ -1283,8 +1402,11 @@ int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t l
           : XFT_CLU_PROMO == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return XFT_ENOTSUP;
-  auto kern = xft_colclu_kernel<Cfg>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM) != cudaSuccess)
+  void (*kern)(const CUtensorMap, C*, long long, int, ColChirp, const double2*, const double2*, const C*);
+  if constexpr (BULK) kern = xft_colclu2_kernel<Cfg>;
+  else kern = xft_colclu_kernel<Cfg>;
+  const size_t smem = BULK ? (2 * (size_t)Cfg::BUF + (size_t)Cfg::L * W) * sizeof(C) : Cfg::SMEM;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return XFT_ECUDA;
   if (K > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     cudaGetLastError();
@@ -1298,7 +1420,7 @@ int launch_colclu(const void* in, void* out, int64_t R, int64_t ncols, int64_t l
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(Cfg::THREADS);
-  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
@@ -1328,7 +1450,11 @@ int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_
 #if XFT_CLU14 == 1
     case 14: return launch_colclu<C, 8, 11, W / 2, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
 #else
-    case 14: return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
+    case 14:
+      if constexpr (sizeof(C) == 8 && XFT_CLU_BULK && W == 8)
+        return launch_colclu<C, 16, 10, W, 1, 1, true>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
+      else
+        return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
 #endif
     case 13: return launch_colclu<C, 8, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
     case 12: return launch_colclu<C, 4, 10, W>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
