@@ -1258,7 +1258,8 @@ xft_colclu_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __re
 // One CTA per SM (two group buffers + the receive buffer: ~200 KB).
 // ---------------------------------------------------------------------------
 #ifndef XFT_CLU_BULK
-#define XFT_CLU_BULK 1  // c64 16-CTA column clusters with the copy-engine exchange (K6b)
+#define XFT_CLU_BULK 0  // 1: c64 16-CTA column clusters with the copy-engine exchange (K6b). A/B cfg5:
+                        // 3.35 ms (W = 8, one CTA/SM), 3.03 ms (W = 4, two/SM) vs 2.81 ms for K6: off
 #endif
 __device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint32_t mbar_cluster) {
   asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -1270,7 +1271,7 @@ __device__ __forceinline__ void clu_arrive() { asm volatile("barrier.cluster.arr
 __device__ __forceinline__ void clu_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 1)
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 xft_colclu2_kernel(const __grid_constant__ CUtensorMap map, typename Cfg::C* __restrict__ out, long long ld,
                    int ngroups, ColChirp ck, const double2* __restrict__ ptab, const double2* __restrict__ cptab,
                    const typename Cfg::C* __restrict__ tw) {
@@ -1451,8 +1452,9 @@ int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_
     case 14: return launch_colclu<C, 8, 11, W / 2, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
 #else
     case 14:
-      if constexpr (sizeof(C) == 8 && XFT_CLU_BULK && W == 8)
-        return launch_colclu<C, 16, 10, W, 1, 1, true>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
+      if constexpr (sizeof(C) == 8 && XFT_CLU_BULK && (W == 8 || W == 4))
+        return launch_colclu<C, 16, 10, W, 1, (W == 4 ? 2 : 1), true>(in, out, R, ncols, ld, ck, ptab, cptab, st,
+                                                                        ld_out, probe);
       else
         return launch_colclu<C, 16, 10, W, XFT_CLU_NB, XFT_CLU_MINB>(in, out, R, ncols, ld, ck, ptab, cptab, st, ld_out, probe);
 #endif
