@@ -22,3 +22,9 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("cfg2")
+    # the same `config` dict as the GPU arm's line (the driver compares the two)
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert d["config"] == bench.workload_config(bench.make_workload("cfg2")[1])
+    assert d["cpu_baseline"]["kind"] == "reference" or not os.path.isdir(os.path.join(ROOT, "oracle", "_ref"))
