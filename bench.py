@@ -578,10 +578,13 @@ def measure_e2e(work, sets, launch, dev, args, world, samples_job, barrier, max_
             "api": "ops.lct_host -> xft_lct_host" if work[0].kind == "lct" else "pinned H2D + public op + D2H"}
 
 
-FP64_ALG_FLOPS = {  # algorithmic fp64 flops per output sample of a c128 row (5 n log2 n FFT + 2 complex products)
+FP64_ALG_FLOPS = {  # nominal fp64 flops per output sample of a c128 row
+    # fast LCT: one length-n FFT (5 n log2 n) + the two chirp products (6 + 6)
     "lct": lambda n: 5.0 * np.log2(n) + 12.0,
-    # Mehler rows: 3 length-M FFTs (M ~ 2n windowed) + 3 complex products per sample
-    "mehler": lambda n: 3 * 5.0 * np.log2(2 * n) * 2 + 18.0,
+    # Mehler apply (the kernel spectrum is part of the plan): two length-2n FFTs per row
+    # (2 x 5 (2n) log2(2n) / n) + input weight, spectrum and output weight products (6 + 12 + 6);
+    # the per-row windows make the true M smaller on most rows, so this overstates the work
+    "mehler": lambda n: 20.0 * np.log2(2 * n) + 24.0,
 }
 
 
