@@ -1465,6 +1465,8 @@ int lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, int64_
   }
 }
 
+#include "xft_colring.cuh"
+
 #ifndef XFT_COLSLAB_MB
 #define XFT_COLSLAB_MB 4096  // L2-resident scratch per column slab (4096: one slab; smaller slabs measured slower)
 #endif
@@ -1482,6 +1484,10 @@ int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int6
     const double2 *ptab = nullptr, *cptab = nullptr;
     int rc = boundary_tables(R, &ptab, &cptab);
     if (rc) return rc;
+    if constexpr (sizeof(C) == 8) {  // c64, 2^12 .. 2^16 rows: two passes through an L2-resident ring (K7)
+      rc = lct_cols_ring(in, out, R, ncols, ld, ld, k, st);
+      if (rc != XFT_ENOTSUP) return rc;
+    }
     rc = lct_cols_cluster<C>(in, out, R, ncols, ld, k, ptab, cptab, st);
     if (rc != XFT_ENOTSUP) return rc;
   }
@@ -1531,6 +1537,14 @@ int run_lct_cols_cluster(const void* in, void* out, int64_t R, int64_t ncols, in
   if (rc) return rc;
   return dtype == XFT_C64 ? lct_cols_cluster<float2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out, probe)
                           : lct_cols_cluster<double2>(in, out, R, ncols, ld, k, ptab, cptab, st, ld_out, probe);
+}
+
+// true when the L2-staged column path (K7) takes this shape on this device (nothing launched)
+bool lct_cols_ring_ok(const void* in, int64_t R, int64_t ncols, int64_t ld, int dtype) {
+  const int l = log2_of(R);
+  if (dtype != XFT_C64 || (int64_t(1) << l) != R) return false;
+  ColChirp k{};
+  return lct_cols_ring(in, nullptr, R, ncols, ld, ld, k, nullptr, true) == XFT_OK;
 }
 
 int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, int dtype,

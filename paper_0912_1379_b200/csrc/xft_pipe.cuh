@@ -437,8 +437,12 @@ using ChirpTurnWalk = std::conditional_t<XFT_WALK32 != 0, TurnWalk32, TurnWalk>;
 // ---------------------------------------------------------------------------
 // configuration
 // ---------------------------------------------------------------------------
-template <class C_, int LOG2N_, int E_, int MODE_, int SIGN_, int ROWS_, int STAGES_, int MINB_, int SPLITOK_ = 0>
+template <class C_, int LOG2N_, int E_, int MODE_, int SIGN_, int ROWS_, int STAGES_, int MINB_, int SPLITOK_ = 0,
+          int BARTH_ = 0>
 struct PipeCfg {
+  // threads that take part in the exchange barriers: 0 = the whole CTA (__syncthreads), else a named
+  // barrier over the first BARTH threads (kernels with extra, non-computing warps)
+  static constexpr int BARTH = BARTH_;
   using C = C_;
   using Coef = typename CoefOf<C>::T;
   static constexpr int LOG2N = LOG2N_, N = 1 << LOG2N, E = E_, MODE = MODE_, SIGN = SIGN_;
@@ -521,6 +525,12 @@ __device__ __forceinline__ constexpr int pad_idx(int a) { return a + (a >> 4); }
 #ifndef XFT_TWPRE
 #define XFT_TWPRE 0  // 1: load the next pass's twiddles between the exchange stores and the barrier
 #endif
+template <class Cfg>
+__device__ __forceinline__ void pipe_sync() {
+  if constexpr (Cfg::BARTH > 0) named_sync(1, Cfg::BARTH);
+  else __syncthreads();
+}
+
 template <class Cfg, int P, bool FREE_EARLY, class Release, class Free>
 __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
                                           const typename Cfg::C* __restrict__ tw, Release&& release,
@@ -632,7 +642,7 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     for (int t = 0; t < R; ++t) v[b + t * NB] = u[t];
   }
   if constexpr (!LAST) {
-    __syncthreads();  // every thread is done reading this buffer
+    pipe_sync<Cfg>();  // every thread is done reading this buffer
     if constexpr (P == 0) release();  // (first-barrier hook)
     // Stockham store: element t of butterfly i goes to base + t NS, base =
     // (i - k) R + k.  (base mod 16) + (t NS mod 16) < 16 for every thread (NS
@@ -656,13 +666,13 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
         for (int t = 1; t < E; ++t) wpre[t - 1] = __ldg(twp + (t - 1) * NS1);
       }
     }
-    __syncthreads();
+    pipe_sync<Cfg>();
     // j < TR and TR | 16 or 16 | TR: pad_idx(j + s TR) = pad_idx(j) + s TR + (s TR) / 16
     const C* src = rs + pad_idx(j);
 #pragma unroll
     for (int s = 0; s < E; ++s) v[s] = src[s * TR + ((s * TR) >> 4)];
     if constexpr (FREE_EARLY && P == Cfg::NPASS - 2) {
-      __syncthreads();
+      pipe_sync<Cfg>();
       free_hook();
     }
   }
