@@ -24,20 +24,41 @@
 #pragma once
 
 #ifndef XFT_RING_SB
-#define XFT_RING_SB 2      // column blocks handed out side by side (SB x 128 B contiguous per row)
+#define XFT_RING_SB 1      // column blocks handed out side by side (SB x 128 B contiguous per row)
 #endif
 #ifndef XFT_RING_LAG
-#define XFT_RING_LAG 4     // super-blocks between a block's pass 1 and its pass 2
+#define XFT_RING_LAG 3     // super-blocks between a block's pass 1 and its pass 2
 #endif
 #ifndef XFT_RING_SLOTS
-#define XFT_RING_SLOTS 8   // ring slots (super-blocks of scratch)
+#define XFT_RING_SLOTS 6   // ring slots (super-blocks of scratch)
 #endif
 #ifndef XFT_RING_STAGES
-#define XFT_RING_STAGES 2  // TMA stages per CTA
+#define XFT_RING_STAGES 3  // TMA stages per CTA
+#endif
+#ifndef XFT_RING_W
+#define XFT_RING_W 64      // columns per tile up to 128 rows a pass (512-byte row segments); a quarter of it beyond
+#endif
+#ifndef XFT_RING_TR
+#define XFT_RING_TR 8      // threads per column (each holds L / TR samples)
 #endif
 #ifndef XFT_RING_MINB
-#define XFT_RING_MINB 4    // resident CTAs per SM the registers are sized for
+#define XFT_RING_MINB (64 / XFT_RING_W)  // resident CTAs per SM the registers are sized for (full-width tiles)
 #endif
+#ifndef XFT_RING_STATIC
+#define XFT_RING_STATIC 1  // 1: CTA b takes tiles b, b + grid, ... (cooperative launch: every CTA is resident);
+#endif                     // 0: a global ticket counter (one same-address atomic per tile: measured the bottleneck)
+#ifndef XFT_RING_QUEUE
+#define XFT_RING_QUEUE 2   // tiles a CTA looks ahead beyond its unsignalled ones
+#endif
+#ifndef XFT_RING_NSUB
+#define XFT_RING_NSUB 8    // completion sub-counters per (pass, super-block), 256 B apart (different L2 slices):
+#endif                     // same-address atomics complete at ~1 per 4-8 ns, a block finishes 256 tiles in ~1 us
+#ifndef XFT_RING_DONE
+#define XFT_RING_DONE 8    // completion barriers per CTA: tiles computed but not yet signalled
+#endif
+#ifndef XFT_RING_ABL
+#define XFT_RING_ABL 0     // timing experiments only (wrong results): 1 = pass 1 alone, 2 = pass 2 alone (no waits),
+#endif                     // 4 = no FFT passes (data movement only); bits may be combined
 #ifndef XFT_COLRING
 #define XFT_COLRING 1      // 0: never take the L2-staged column path
 #endif
@@ -49,6 +70,7 @@ struct RingPlan {
   int R1, R2, nblocks, SB, nsb, lag, slots;
   unsigned T0, T1;        // tiles per super-block: pass 1 (SB R2), pass 2 (SB R1)
   unsigned tA, tB, total; // ticket regions: leading pass-1 only, interleaved, trailing pass-2 only
+  int l0, l1, lsb;        // log2 of T0, T1, SB (all powers of two: the decode below uses shifts only)
   long long ld_in, ld_out;
   int ncols;
 };
@@ -66,33 +88,61 @@ __device__ __forceinline__ RingTile ring_decode(const RingPlan& p, unsigned tk) 
     return t;
   }
   unsigned off;
+  if (XFT_RING_ABL & 3) {  // one pass alone over every block
+    const int l = (XFT_RING_ABL & 1) ? p.l0 : p.l1;
+    t.phase = (XFT_RING_ABL & 1) ? 0 : 1;
+    t.sb = (int)(tk >> l);
+    off = tk & ((1u << l) - 1);
+    t.idx = (int)(off >> p.lsb);
+    t.cb = (t.sb << p.lsb) + (int)(off & ((1u << p.lsb) - 1));
+    return t;
+  }
   if (tk < p.tA) {
     t.phase = 0;
-    t.sb = (int)(tk / p.T0);
-    off = tk % p.T0;
+    t.sb = (int)(tk >> p.l0);
+    off = tk & (p.T0 - 1);
   } else if (tk < p.tA + p.tB) {
-    const unsigned u = tk - p.tA, per = p.T0 + p.T1;
-    const int m = (int)(u / per);
-    off = u % per;
+    // one pass-1 block-phase (T0 tiles) then one pass-2 block-phase (T1 = T0 or 2 T0 tiles)
+    const unsigned u = tk - p.tA;
+    const unsigned m = p.l1 == p.l0 ? u >> (p.l0 + 1) : (u >> p.l0) / 3u;
+    off = u - m * (p.T0 + p.T1);
     if (off < p.T0) {
       t.phase = 0;
-      t.sb = p.lag + m;
+      t.sb = p.lag + (int)m;
     } else {
       t.phase = 1;
-      t.sb = m;
+      t.sb = (int)m;
       off -= p.T0;
     }
   } else {
     const unsigned u = tk - p.tA - p.tB;
     t.phase = 1;
-    t.sb = p.nsb - p.lag + (int)(u / p.T1);
-    off = u % p.T1;
+    t.sb = p.nsb - p.lag + (int)(u >> p.l1);
+    off = u & (p.T1 - 1);
   }
-  t.idx = (int)(off / p.SB);
-  t.cb = t.sb * p.SB + (int)(off % p.SB);
+  t.idx = (int)(off >> p.lsb);
+  t.cb = (t.sb << p.lsb) + (int)(off & ((1u << p.lsb) - 1));
   return t;
 }
 
+constexpr int RING_CSTRIDE = 64;  // words between sub-counters (256 B: the L2 slice hash granularity)
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// every sub-counter of a (pass, super-block) has reached `want`: relaxed loads in flight together,
+// then one acquire fence
+__device__ __forceinline__ bool ring_complete(const unsigned* ctr, unsigned want) {
+  unsigned v[XFT_RING_NSUB];
+#pragma unroll
+  for (int u = 0; u < XFT_RING_NSUB; ++u) v[u] = ld_relaxed_gpu(ctr + u * RING_CSTRIDE);
+  bool ok = true;
+#pragma unroll
+  for (int u = 0; u < XFT_RING_NSUB; ++u) ok = ok && v[u] >= want;
+  if (ok) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  return ok;
+}
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -139,17 +189,20 @@ template <int LOG1_, int LOG2_>
 struct RingCfg {
   using C = float2;
   static constexpr int LOG1 = LOG1_, LOG2 = LOG2_, R1 = 1 << LOG1, R2 = 1 << LOG2;
-  static constexpr int W = 16, TR = 8, THREADS = W * TR;
+  static constexpr int LMAXR = R1 > R2 ? R1 : R2;
+  static constexpr int W = LMAXR <= 128 ? XFT_RING_W : XFT_RING_W / 4, TR = XFT_RING_TR, THREADS = W * TR;
+  static constexpr int MINB = LMAXR <= 128 ? XFT_RING_MINB : (XFT_RING_W >= 64 ? 2 : 1);
   static constexpr int E1 = R1 / TR, E2 = R2 / TR;
   using Fft1 = PipeCfg<C, LOG1, E1, MODE_DFT, -1, W, 1, 1, 0, THREADS>;  // exchange barriers: the compute warps only
   using Fft2 = PipeCfg<C, LOG2, E2, MODE_DFT, -1, W, 1, 1, 0, THREADS>;
-  static constexpr int LMAXR = R1 > R2 ? R1 : R2;
   static constexpr int NPMAX = LMAXR + LMAXR / 16;
   static constexpr int LS = NPMAX + (((1 - NPMAX % 16) % 16) + 16) % 16;  // == 1 (mod 16): W lines x 1 slot per wavefront
-  static constexpr int NS = XFT_RING_STAGES;
-  // stage: [L][W] tile, then two table rows of L entries
-  static constexpr int STAGE = LMAXR * W + 2 * LMAXR;
-  static constexpr size_t SMEM = (size_t(NS) * STAGE + size_t(W) * LS) * sizeof(C);
+  // stages; completion barriers (tiles whose stores may still be unsignalled); tile-info slots
+  static constexpr int NS = XFT_RING_STAGES, ND = XFT_RING_DONE, NI = ND + XFT_RING_QUEUE;
+  // stage: [L][W] tile, then two table rows of L entries; later the tile's padded exchange buffer [W][LS]
+  static constexpr int STAGE0 = LMAXR * W + 2 * LMAXR > W * LS ? LMAXR * W + 2 * LMAXR : W * LS;
+  static constexpr int STAGE = (STAGE0 + 15) / 16 * 16;
+  static constexpr size_t SMEM = size_t(NS) * STAGE * sizeof(C);
 };
 
 // table rows + counters for one call (stream scratch), written by ring_setup_kernel:
@@ -159,8 +212,8 @@ struct RingBufs {
   const float2* pre;
   const float2* post;
   const float2* twr;    // [r2][k1] = w_R^{k1 r2} (per device and R)
-  unsigned* ticket;     // [0] = ticket, then done1[nsb], done2[nsb]
-  unsigned* done1;
+  unsigned* ticket;     // the ticket counter (XFT_RING_STATIC = 0), 256 B before the completion counters
+  unsigned* done1;      // [nsb][NSUB] sub-counters, RING_CSTRIDE words apart; tile idx counts on idx % NSUB
   unsigned* done2;
 };
 
@@ -208,30 +261,41 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void red_release_gpu(unsigned* p) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+  if (XFT_RING_ABL & 8) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+  else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
 
-// One scheduler warp (lane 0) + THREADS compute threads.  The scheduler takes tickets, checks the
-// tile's dependency counter, issues the tile's bulk copies and publishes completion counters; the
-// compute warps only ever wait on shared-memory mbarriers:
-//   full[s]  scheduler -> compute: tile (or the end marker) of sequence number q, s = q % NS, has landed
-//   done[s]  compute -> scheduler: every compute thread has issued the tile's stores
-// Sequence q + NS is fetched and issued only after q has been signalled, so a stage, its info
-// slot and both barriers are reused strictly one phase at a time.  The scheduler never blocks: a
-// tile whose dependency is not yet satisfied just stays pending while completions are published,
-// which (with the ticket order) rules out deadlock.
+// Warp roles: THREADS compute threads, one issuer warp, one signaller warp (lane 0 of each).
+//   issuer     takes tickets ahead (XFT_RING_QUEUE beyond the stages), checks each tile's
+//              dependency counter ahead of time, and issues the tile's bulk copies as soon as its
+//              stage is free -- nothing with a global round trip sits between "stage free" and
+//              the TMA issue;
+//   signaller  waits for done[s] of sequence q and publishes the tile's completion (one
+//              red.release at GPU scope), then advances `nsig` (shared);
+//   compute    waits on full[s], transforms, stores, arrives on done[s].
+// Barriers:  full[s]   issuer -> compute: the tile (or the end marker) of sequence q, s = q % NS, has landed
+//            empty[s]  compute -> issuer: the last shared-memory read of the tile is done (before its stores)
+//            done[d]   compute -> signaller: every compute thread has issued the tile's stores, d = q % ND
+// Sequence q is issued only once q - NS has released its stage and q - ND has been signalled, so
+// stages, barriers and info slots are reused strictly one phase at a time, while a stage is NOT
+// held for the store-drain and signal latencies of its tile.  Neither helper blocks on a dependency: a tile
+// whose counter is not yet complete stays pending while completions keep being published, which
+// (with the ticket order) rules out deadlock.
+// The Stockham exchange of a tile runs inside its own stage (the tile and its table rows are in
+// registers by then), so a CTA needs NS x 18.5 KB of shared memory.
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS + 32, XFT_RING_MINB)
+__global__ void __launch_bounds__(Cfg::THREADS + 64, Cfg::MINB)
 xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__ out, RingPlan pl, RingBufs bf,
                    const float2* __restrict__ tw1, const float2* __restrict__ tw2) {
   using C = float2;
-  constexpr int W = Cfg::W, TR = Cfg::TR, NS = Cfg::NS, R1 = Cfg::R1, R2 = Cfg::R2;
+  constexpr int W = Cfg::W, TR = Cfg::TR, NS = Cfg::NS, ND = Cfg::ND, NI = Cfg::NI, R1 = Cfg::R1, R2 = Cfg::R2;
   extern __shared__ __align__(128) unsigned char xft_smem[];
   __shared__ __align__(8) uint64_t full[NS];
-  __shared__ __align__(8) uint64_t done[NS];
-  __shared__ RingTile info[NS];
+  __shared__ __align__(8) uint64_t empty[NS];
+  __shared__ __align__(8) uint64_t done[ND];
+  __shared__ RingTile info[NI];
+  __shared__ volatile int nsig;  // sequences signalled so far (signaller -> issuer)
   C* const stages = reinterpret_cast<C*>(xft_smem);
-  C* const xbuf = stages + NS * Cfg::STAGE;
   const int t = threadIdx.x;
   const long long R = (long long)R1 * R2;
   auto slot_base = [&](const RingTile& ti) -> C* {
@@ -242,82 +306,99 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&done[s], Cfg::THREADS);
+      mbar_init(&empty[s], Cfg::THREADS);
     }
+#pragma unroll
+    for (int s = 0; s < ND; ++s) mbar_init(&done[s], Cfg::THREADS);
+    nsig = 0;
     fence_mbar_init();
   }
   __syncthreads();
 
+  if (t >= Cfg::THREADS + 32) {
+    // ------------------------------ signaller ------------------------------
+    if (t != Cfg::THREADS + 32) return;
+    for (int q = 0;; ++q) {
+      mbar_wait(&done[q % ND], (uint32_t)((q / ND) & 1));
+      const RingTile ti = info[q % NI];
+      if (ti.phase == 2) break;
+      red_release_gpu((ti.phase == 0 ? bf.done1 : bf.done2) +
+                      ((long long)ti.sb * XFT_RING_NSUB + ti.idx % XFT_RING_NSUB) * RING_CSTRIDE);
+      nsig = q + 1;
+    }
+    return;
+  }
   if (t >= Cfg::THREADS) {
-    // ------------------------------ scheduler ------------------------------
+    // ------------------------------ issuer ------------------------------
     if (t != Cfg::THREADS) return;
     const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
-    int nf = 0, ni = 0, nsg = 0, nreal = 0x7fffffff;
+    // tickets fetched; dependencies verified; tiles issued (incl. the end marker); stage releases observed
+    int nf = 0, nd = 0, ni = 0, nrel = 0;
     bool ended = false;
-    const unsigned* ok_ctr = nullptr;  // the last dependency counter seen satisfied (acquired once per CTA)
+    const unsigned* ok_ctr = nullptr;  // the last dependency counter seen complete
     unsigned long long idle_since = 0;
     while (true) {
       bool progress = false;
-      if (nsg < ni && nsg < nreal && mbar_test(&done[nsg % NS], (uint32_t)((nsg / NS) & 1))) {
-        const RingTile ti = info[nsg % NS];
-        red_release_gpu((ti.phase == 0 ? bf.done1 : bf.done2) + ti.sb);
-        ++nsg;
-        progress = true;
-      }
-      if (!ended && nf < nsg + NS) {
-        const unsigned tk = atomicAdd(bf.ticket, 1u);
+      const int sg = nsig;
+      if (!ended && nf < sg + NI) {
+        const unsigned tk = XFT_RING_STATIC ? blockIdx.x + (unsigned)nf * gridDim.x : atomicAdd(bf.ticket, 1u);
         const RingTile ti = ring_decode(pl, tk);
-        info[nf % NS] = ti;
-        if (ti.phase == 2) {
-          ended = true;
-          nreal = nf;
-        }
+        info[nf % NI] = ti;
+        if (ti.phase == 2) ended = true;
         ++nf;
         progress = true;
       }
-      if (ni < nf) {
-        const int st = ni % NS;
-        const RingTile ti = info[st];
-        if (ti.phase == 2) {
-          mbar_arrive(&full[st]);  // end marker: the compute warps wake up, read it and leave
-          ++ni;
+      if (nd < nf) {  // the oldest tile whose dependency is still unverified
+        const RingTile ti = info[nd % NI];
+        const unsigned* ctr = nullptr;
+        unsigned want = 0;
+        if (ti.phase == 0) {
+          if (ti.sb >= pl.slots) {
+            ctr = bf.done2 + (long long)(ti.sb - pl.slots) * XFT_RING_NSUB * RING_CSTRIDE;
+            want = pl.T1 / XFT_RING_NSUB;
+          }
+        } else if (ti.phase == 1) {
+          ctr = bf.done1 + (long long)ti.sb * XFT_RING_NSUB * RING_CSTRIDE;
+          want = pl.T0 / XFT_RING_NSUB;
+        }
+        if (XFT_RING_ABL & 3) ctr = nullptr;
+        if (ctr == nullptr || ctr == ok_ctr) {
+          ++nd;
           progress = true;
-        } else {
-          const unsigned* ctr = nullptr;
-          unsigned want = 0;
-          if (ti.phase == 0) {
-            if (ti.sb >= pl.slots) {
-              ctr = bf.done2 + (ti.sb - pl.slots);
-              want = pl.T1;
-            }
-          } else {
-            ctr = bf.done1 + ti.sb;
-            want = pl.T0;
-          }
-          if (ctr == nullptr || ctr == ok_ctr || ld_acquire_gpu(ctr) >= want) {
-            if (ctr) ok_ctr = ctr;
-            C* const S = stages + st * Cfg::STAGE;
-            fence_proxy_async_all();  // the stage's generic-proxy reads; (pass 2) the acquired scratch stores
-            if (ti.phase == 0) {
-              mbar_arrive_expect_tx(&full[st], (uint32_t)((R1 * W + 2 * R1) * sizeof(C)));
-              if (XFT_RING_HINT) tma_load_3d_hint(S, &map, ti.cb * W, ti.idx, 0, &full[st], pol_first);
-              else tma_load_3d(S, &map, ti.cb * W, ti.idx, 0, &full[st]);
-              tma_load_1d(S + Cfg::LMAXR * W, bf.pre + (long long)ti.idx * R1, R1 * sizeof(C), &full[st]);
-              tma_load_1d(S + Cfg::LMAXR * W + Cfg::LMAXR, bf.twr + (long long)ti.idx * R1, R1 * sizeof(C),
-                          &full[st]);
-            } else {
-              mbar_arrive_expect_tx(&full[st], (uint32_t)((R2 * W + R2) * sizeof(C)));
-              const C* src = slot_base(ti) + (long long)ti.idx * R2 * W;
-              if (XFT_RING_HINT) tma_load_1d_hint(S, src, R2 * W * sizeof(C), &full[st], pol_last);
-              else tma_load_1d(S, src, R2 * W * sizeof(C), &full[st]);
-              tma_load_1d(S + Cfg::LMAXR * W, bf.post + (long long)ti.idx * R2, R2 * sizeof(C), &full[st]);
-            }
-            ++ni;
-            progress = true;
-          }
+        } else if (ring_complete(ctr, want)) {
+          ok_ctr = ctr;
+          fence_proxy_async_all();  // the acquired generic-proxy stores (scratch) are read by bulk copies
+          ++nd;
+          progress = true;
         }
       }
-      if (ended && ni == nf && nsg >= nreal) break;
+      if (nrel < ni && mbar_test(&empty[nrel % NS], (uint32_t)((nrel / NS) & 1))) {
+        ++nrel;  // the compute warps have read the last shared-memory word of sequence nrel's stage
+        progress = true;
+      }
+      if (ni < nd && ni < nrel + NS && ni < sg + ND) {
+        const int st = ni % NS;
+        const RingTile ti = info[ni % NI];
+        C* const S = stages + st * Cfg::STAGE;
+        if (ti.phase == 2 || (XFT_RING_ABL & 128)) {
+          mbar_arrive(&full[st]);  // end marker: the compute warps wake up, read it and leave
+        } else if (ti.phase == 0) {
+          mbar_arrive_expect_tx(&full[st], (uint32_t)((R1 * W + 2 * R1) * sizeof(C)));
+          if (XFT_RING_HINT) tma_load_3d_hint(S, &map, ti.cb * W, ti.idx, 0, &full[st], pol_first);
+          else tma_load_3d(S, &map, ti.cb * W, ti.idx, 0, &full[st]);
+          tma_load_1d(S + Cfg::LMAXR * W, bf.pre + (long long)ti.idx * R1, R1 * sizeof(C), &full[st]);
+          tma_load_1d(S + Cfg::LMAXR * W + Cfg::LMAXR, bf.twr + (long long)ti.idx * R1, R1 * sizeof(C), &full[st]);
+        } else {
+          mbar_arrive_expect_tx(&full[st], (uint32_t)((R2 * W + R2) * sizeof(C)));
+          const C* src = slot_base(ti) + (long long)ti.idx * R2 * W;
+          if (XFT_RING_HINT) tma_load_1d_hint(S, src, R2 * W * sizeof(C), &full[st], pol_last);
+          else tma_load_1d(S, src, R2 * W * sizeof(C), &full[st]);
+          tma_load_1d(S + Cfg::LMAXR * W, bf.post + (long long)ti.idx * R2, R2 * sizeof(C), &full[st]);
+        }
+        ++ni;
+        progress = true;
+        if (ti.phase == 2) break;
+      }
       if (progress) {
         idle_since = 0;
       } else {
@@ -326,7 +407,7 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
         const unsigned long long now = global_ns();
         if (idle_since == 0) idle_since = now;
         else if (now - idle_since > 4000000000ull) __trap();
-        __nanosleep(40);
+        __nanosleep(64);
       }
     }
     return;
@@ -339,8 +420,11 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
   for (int i = 0;; ++i) {
     const int st = i % NS;
     mbar_wait(&full[st], (uint32_t)((i / NS) & 1));
-    const RingTile ti = info[st];
-    if (ti.phase == 2) break;
+    const RingTile ti = info[i % NI];
+    if (ti.phase == 2) {
+      mbar_arrive(&done[i % ND]);  // lets the signaller see the end marker
+      break;
+    }
     C* const S = stages + st * Cfg::STAGE;
     const int col = ti.cb * W + w;
     if (ti.phase == 0) {
@@ -354,12 +438,14 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
         v[s] = cmul(pre[a], S[a * W + w]);
         tq[s] = twr[a];
       }
-      pipe_passes<typename Cfg::Fft1, 0>(v, xbuf + w * Cfg::LS, j, tw1, noop);
+      if (!(XFT_RING_ABL & 4)) pipe_passes<typename Cfg::Fft1, 0>(v, S + w * Cfg::LS, j, tw1, noop);
+      mbar_arrive(&empty[st]);  // this thread is done with the stage
       C* dst = slot_base(ti) + (long long)ti.idx * W + w;
 #pragma unroll
       for (int s = 0; s < E; ++s) {
         const int k1 = j + s * TR;
         const C y = cmul(v[s], tq[s]);
+        if ((XFT_RING_ABL & 64) && y.x != 123.f) continue;
         if (XFT_RING_HINT) st_hint(dst + (long long)k1 * R2 * W, y, pol_last);
         else dst[(long long)k1 * R2 * W] = y;
       }
@@ -374,17 +460,19 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
         v[s] = S[a * W + w];
         pq[s] = post[a];
       }
-      pipe_passes<typename Cfg::Fft2, 0>(v, xbuf + w * Cfg::LS, j, tw2, noop);
+      if (!(XFT_RING_ABL & 4)) pipe_passes<typename Cfg::Fft2, 0>(v, S + w * Cfg::LS, j, tw2, noop);
+      mbar_arrive(&empty[st]);
       if (col < pl.ncols) {
         C* dst = out + (long long)ti.idx * pl.ld_out + col;
 #pragma unroll
         for (int s = 0; s < E; ++s) {
           const int k2 = j + s * TR;
+          if ((XFT_RING_ABL & 64) && v[s].x != 123.f) continue;
           st_stream(dst + (long long)k2 * R1 * pl.ld_out, cmul(v[s], pq[s]));
         }
       }
     }
-    mbar_arrive(&done[st]);
+    mbar_arrive(&done[i % ND]);
   }
 }
 
@@ -433,7 +521,7 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::THREADS + 32, Cfg::SMEM) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::THREADS + 64, Cfg::SMEM) != cudaSuccess ||
       occ < 1) {
     cudaGetLastError();
     return XFT_ENOTSUP;
@@ -450,17 +538,22 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   pl.slots = pl.nsb < XFT_RING_SLOTS ? pl.nsb : XFT_RING_SLOTS;
   pl.T0 = (unsigned)(pl.SB * R2);
   pl.T1 = (unsigned)(pl.SB * R1);
+  pl.lsb = log2_of(pl.SB);
+  pl.l0 = pl.lsb + LOG2;
+  pl.l1 = pl.lsb + LOG1;
+  static_assert(LOG1 == LOG2 || LOG1 == LOG2 + 1, "pass-2 block-phases are 1x or 2x the pass-1 ones");
   pl.tA = (unsigned)pl.lag * pl.T0;
   pl.tB = (unsigned)(pl.nsb - pl.lag) * (pl.T0 + pl.T1);
   pl.total = pl.tA + pl.tB + (unsigned)pl.lag * pl.T1;
+  if (XFT_RING_ABL & 3) pl.total = (unsigned)pl.nsb * ((XFT_RING_ABL & 1) ? pl.T0 : pl.T1);
   pl.ld_in = ld;
   pl.ld_out = ld_out;
   pl.ncols = (int)ncols;
   // scratch: ring, pre/post table rows, counters
   const size_t ring_bytes = (size_t)pl.slots * pl.SB * R * W * sizeof(float2);
   const size_t tab_bytes = (size_t)R * sizeof(float2);
-  const int ncounters = 1 + 2 * pl.nsb;
-  const size_t ctr_bytes = ((size_t)ncounters * 4 + 255) / 256 * 256;
+  const int ncounters = RING_CSTRIDE * (1 + 2 * pl.nsb * XFT_RING_NSUB);
+  const size_t ctr_bytes = (size_t)ncounters * 4;
   char* base = static_cast<char*>(stream_scratch(dev, st, ring_bytes + 2 * tab_bytes + ctr_bytes));
   if (!base) return XFT_ECUDA;
   RingBufs bf{};
@@ -470,8 +563,8 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   bf.pre = pre;
   bf.post = post;
   bf.ticket = reinterpret_cast<unsigned*>(base + ring_bytes + 2 * tab_bytes);
-  bf.done1 = bf.ticket + 1;
-  bf.done2 = bf.done1 + pl.nsb;
+  bf.done1 = bf.ticket + RING_CSTRIDE;
+  bf.done2 = bf.done1 + (size_t)pl.nsb * XFT_RING_NSUB * RING_CSTRIDE;
   int rc = ring_twiddles(LOG1, LOG2, &bf.twr);
   if (rc) return rc;
   Tables t1, t2;
@@ -479,7 +572,9 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   if ((rc = get_tables(R2, XFT_C64, &t2, Cfg::E2))) return rc;
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)ncols, (cuuint64_t)R2, (cuuint64_t)R1};
-  const cuuint64_t strides[2] = {(cuuint64_t)(ld * sizeof(float2)), (cuuint64_t)(R2 * ld * sizeof(float2))};
+  // (XFT_RING_ABL & 32: a tile = R1 CONSECUTIVE rows -- wrong rows, the access-pattern experiment)
+  const cuuint64_t strides[2] = {(cuuint64_t)(((XFT_RING_ABL & 32) ? R1 : 1) * ld * sizeof(float2)),
+                                 (cuuint64_t)(((XFT_RING_ABL & 32) ? 1 : R2) * ld * sizeof(float2))};
   const cuuint32_t box[3] = {(cuuint32_t)W, 1u, (cuuint32_t)R1};
   const cuuint32_t estr[3] = {1u, 1u, 1u};
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<void*>(in), dims, strides, box, estr,
@@ -490,9 +585,24 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   ring_setup_kernel<<<nset, 256, 0, st>>>(pre, post, bf.ticket, ncounters, ck, R1, R2);
   const long long cap = (long long)sms * occ;
   const unsigned grid = (unsigned)(pl.total < cap ? pl.total : cap);
-  kern<<<grid, Cfg::THREADS + 32, Cfg::SMEM, st>>>(map, static_cast<float2*>(out), pl, bf, static_cast<const float2*>(t1.tw),
-                                              static_cast<const float2*>(t2.tw));
-  return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
+  // cooperative launch: the runtime refuses a grid whose CTAs cannot all be resident, which the
+  // static tile assignment relies on (a non-resident CTA would own tiles others wait for)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = XFT_RING_STATIC;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Cfg::THREADS + 64);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, map, static_cast<float2*>(out), pl, bf, static_cast<const float2*>(t1.tw),
+                         static_cast<const float2*>(t2.tw)) != cudaSuccess) {
+    cudaGetLastError();
+    return XFT_ECUDA;
+  }
+  return XFT_OK;
 }
 
 // c64 columns of height 2^12 .. 2^16 (R1 x R2 = 64x64 .. 256x256); anything else: XFT_ENOTSUP, nothing launched
