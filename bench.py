@@ -661,7 +661,7 @@ def run_ours(args, rank, world, local_rank):
                    "cpu_baseline": (cpu_baseline_for(rec["work"], 3.0, 1.5)
                                     if world == 1 and not args.no_cpu else None)}
         if c == "cfg5":
-            cfgs[c]["transport"] = rec["transport"] if world > 1 else "single GPU (rows -> 8 slabs -> columns)"
+            cfgs[c]["transport"] = rec["transport"] if world > 1 else "single GPU (row pass, then columns in place through the L2-resident ring: K7)"
     strong = args.config in ("cfg2", "cfg3", "cfg4") and world > 1
     # `config` names the workload only (identical on the reference arm's line); how it ran is beside it
     line = {

@@ -5,26 +5,42 @@
 // w_R^{k1 r2}; pass 2 = length-R2 DFT over r2, post-chirp, natural row
 // j = k1 + R1 k2.  Run as two kernels the [R][ncols] intermediate crosses HBM
 // twice more.  Here ONE persistent kernel runs both passes over a stream of
-// 16-column "blocks": the pass-1 tiles of a block write a 2 MB slot of a small
-// ring of scratch (tens of MB: it lives in the 126 MB L2), and the pass-2 tiles
-// of the same block are handed out a few blocks later, when every pass-1 tile
-// of the block has signalled (a per-block counter, release/acquire at GPU
-// scope).  The slot is reused once its pass-2 tiles have signalled.  Tiles are
-// handed out by a global ticket in an order in which every tile depends only on
-// tiles with smaller tickets, and a CTA only ever blocks when all its earlier
-// tiles are complete, so the schedule cannot deadlock whatever the residency.
+// W-column "blocks" (W = 64: 512-byte row segments): the pass-1 tiles of a
+// block write one slot of a small ring of scratch (6 slots x 8 MB at R = 16384:
+// it lives in the 126 MB L2), and the pass-2 tiles of the same block follow a
+// few blocks later, once every pass-1 tile of the block has signalled
+// (per-block completion counters, release/acquire at GPU scope).  The slot is
+// reused once its pass-2 tiles have signalled.
 //
-// Data path of a tile (W = 16 columns x L rows, 128-byte row segments):
+// Schedule.  Tiles are numbered so that every tile depends only on tiles with
+// smaller numbers (ring_decode: LAG pass-1 block-phases ahead, then alternating
+// pass-1 / pass-2 block-phases).  CTA b owns tiles b, b + grid, b + 2 grid, ...
+// in that order; the launch is cooperative, so every CTA is resident and the
+// lowest unfinished tile can always run: no deadlock.  (A global ticket
+// counter, XFT_RING_STATIC = 0, needs no residency guarantee but costs one
+// same-address atomic per tile.)  A dependency that never completes would be a
+// bug in the schedule: the issuer traps after 4 s instead of hanging the device.
+//
+// Data path of a tile (W columns x L rows):
 //   TMA (3-D tensor box over the view [R1][R2][ncols] for pass 1, one 1-D bulk
 //   copy of the contiguous [r2][w] scratch tile for pass 2; the tile's chirp /
-//   twiddle table rows ride on the same mbarrier) into a 2-deep stage ring ->
+//   twiddle table rows ride on the same mbarrier) into a 3-deep stage ring ->
 //   registers (L/8 samples per thread, 8 threads per column) -> FFT passes of
-//   the row kernels -> plain coalesced stores (streaming for the output).
-// Every global read is an async bulk copy issued one or two tiles ahead.
+//   the row kernels, exchanging through the tile's own stage -> plain coalesced
+//   stores (evict_last into the ring, streaming for the output).
+// Every global read is an async bulk copy issued by a helper warp tiles ahead;
+// the compute warps wait on shared-memory mbarriers only.
+//
+// Measured (16384^2 c64, B200): 1.26 ms for the column axis (the 16-CTA cluster
+// kernel K6: 1.80 ms), DRAM traffic 2.15 GB read + 2.7-2.9 GB written (4.29 GB
+// algorithmic: part of the ring still leaks to HBM).  Experiments kept as
+// compile-time switches (XFT_RING_ABL): the bare schedule costs 0.20 ms per
+// pass, the FFT arithmetic alone 0.45 ms per pass -- the kernel is bound by
+// FP32 issue + shared-memory instructions at 16 compute warps per SM, not by HBM.
 #pragma once
 
 #ifndef XFT_RING_SB
-#define XFT_RING_SB 1      // column blocks handed out side by side (SB x 128 B contiguous per row)
+#define XFT_RING_SB 1      // column blocks per super-block (the unit of the ring and of the counters)
 #endif
 #ifndef XFT_RING_LAG
 #define XFT_RING_LAG 3     // super-blocks between a block's pass 1 and its pass 2
@@ -51,16 +67,20 @@
 #define XFT_RING_QUEUE 2   // tiles a CTA looks ahead beyond its unsignalled ones
 #endif
 #ifndef XFT_RING_NSUB
-#define XFT_RING_NSUB 8    // completion sub-counters per (pass, super-block), 256 B apart (different L2 slices):
-#endif                     // same-address atomics complete at ~1 per 4-8 ns, a block finishes 256 tiles in ~1 us
+#define XFT_RING_NSUB 8    // completion sub-counters per (pass, super-block), 256 B apart (different L2 slices)
+#endif
 #ifndef XFT_RING_DONE
 #define XFT_RING_DONE 8    // completion barriers per CTA: tiles computed but not yet signalled
 #endif
 #ifndef XFT_RING_ABL
-#define XFT_RING_ABL 0     // timing experiments only (wrong results): 1 = pass 1 alone, 2 = pass 2 alone (no waits),
-#endif                     // 4 = no FFT passes (data movement only); bits may be combined
+#define XFT_RING_ABL 0     // timing experiments only (wrong results), bits: 1 = pass 1 alone, 2 = pass 2 alone (no
+#endif                     // waits), 4 = no FFT passes, 8 = relaxed signals, 32 = consecutive-row tiles, 64 = no stores,
+                           // 128 = no loads
 #ifndef XFT_COLRING
 #define XFT_COLRING 1      // 0: never take the L2-staged column path
+#endif
+#ifndef XFT_RING_PERSIST_MB
+#define XFT_RING_PERSIST_MB 0  // > 0: set the device's persisting-L2 set-aside (cudaLimitPersistingL2CacheSize) once
 #endif
 #ifndef XFT_RING_HINT
 #define XFT_RING_HINT 1    // L2 eviction hints: input evict_first, scratch evict_last
@@ -217,15 +237,17 @@ struct RingBufs {
   unsigned* done2;
 };
 
+// Table rows are stored in the order the threads read them: entry j E + s of a row belongs to
+// sample j + TR s (thread j's register s), so a thread fetches its E entries as E/2 16-byte loads.
 __global__ void ring_setup_kernel(float2* pre, float2* post, unsigned* counters, int ncounters, ColChirp ck, int R1,
-                                  int R2) {
+                                  int R2, int TR) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ncounters) counters[i] = 0u;
   const long long R = (long long)R1 * R2;
   if (i >= R) return;
   const int lr = ck.log2r;
   {  // pre[r2][a], r = a R2 + r2
-    const int r2 = i / R1, a = i % R1;
+    const int r2 = i / R1, e = R1 / TR, a = (i % R1) / e + TR * ((i % R1) % e);
     const long long r = (long long)a * R2 + r2;
     const long long off = 2 * r - R + 1;
     unsigned long long ph = ((unsigned long long)(r & 1) << 63) - ((unsigned long long)r << (63 - lr));
@@ -235,7 +257,7 @@ __global__ void ring_setup_kernel(float2* pre, float2* post, unsigned* counters,
     pre[i] = make_float2((float)c, (float)s);
   }
   {  // post[k1][k2], j = k1 + R1 k2
-    const int k1 = i / R2, k2 = i % R2;
+    const int k1 = i / R2, e = R2 / TR, k2 = (i % R2) / e + TR * ((i % R2) % e);
     const long long j = k1 + (long long)R1 * k2;
     const long long off = 2 * j - R + 1;
     unsigned long long ph = ((unsigned long long)(j & 1) << 63) - ((unsigned long long)j << (63 - lr)) +
@@ -435,8 +457,19 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
 #pragma unroll
       for (int s = 0; s < E; ++s) {
         const int a = j + s * TR;
-        v[s] = cmul(pre[a], S[a * W + w]);
-        tq[s] = twr[a];
+        v[s] = S[a * W + w];
+      }
+      {
+        const float4* p4 = reinterpret_cast<const float4*>(pre + j * E);
+        const float4* t4 = reinterpret_cast<const float4*>(twr + j * E);
+#pragma unroll
+        for (int s = 0; s < E; s += 2) {
+          const float4 p = p4[s / 2], q = t4[s / 2];
+          v[s] = cmul(make_float2(p.x, p.y), v[s]);
+          v[s + 1] = cmul(make_float2(p.z, p.w), v[s + 1]);
+          tq[s] = make_float2(q.x, q.y);
+          tq[s + 1] = make_float2(q.z, q.w);
+        }
       }
       if (!(XFT_RING_ABL & 4)) pipe_passes<typename Cfg::Fft1, 0>(v, S + w * Cfg::LS, j, tw1, noop);
       mbar_arrive(&empty[st]);  // this thread is done with the stage
@@ -458,7 +491,15 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
       for (int s = 0; s < E; ++s) {
         const int a = j + s * TR;
         v[s] = S[a * W + w];
-        pq[s] = post[a];
+      }
+      {
+        const float4* p4 = reinterpret_cast<const float4*>(post + j * E);
+#pragma unroll
+        for (int s = 0; s < E; s += 2) {
+          const float4 p = p4[s / 2];
+          pq[s] = make_float2(p.x, p.y);
+          pq[s + 1] = make_float2(p.z, p.w);
+        }
       }
       if (!(XFT_RING_ABL & 4)) pipe_passes<typename Cfg::Fft2, 0>(v, S + w * Cfg::LS, j, tw2, noop);
       mbar_arrive(&empty[st]);
@@ -478,22 +519,23 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
 
 // (device, R) -> [r2][k1] twiddles w_R^{k1 r2}, R = R1 R2
 std::mutex g_ring_mu;
-std::map<std::tuple<int, int, int>, float2*> g_ring_tw;
-int ring_twiddles(int l1, int l2, const float2** out) {
+std::map<std::tuple<int, int, int, int>, float2*> g_ring_tw;
+int ring_twiddles(int l1, int l2, int TR, const float2** out) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return XFT_ECUDA;
   std::lock_guard<std::mutex> lk(g_ring_mu);
-  auto key = std::make_tuple(dev, l1, l2);
+  auto key = std::make_tuple(dev, l1, l2, TR);
   auto it = g_ring_tw.find(key);
   if (it == g_ring_tw.end()) {
     const int R1 = 1 << l1, R2 = 1 << l2;
     const long long R = (long long)R1 * R2;
     std::vector<float2> h((size_t)R);
+    const int e = R1 / TR;  // thread order within a row: entry j e + s is k1 = j + TR s
     for (int r2 = 0; r2 < R2; ++r2)
       for (int k1 = 0; k1 < R1; ++k1) {
         const long long m = ((long long)k1 * r2) % R;
         const long double th = 2.0L * PI_L * (long double)m / (long double)R;
-        h[(size_t)r2 * R1 + k1] = make_float2((float)cosl(th), (float)-sinl(th));
+        h[(size_t)r2 * R1 + (k1 % TR) * e + k1 / TR] = make_float2((float)cosl(th), (float)-sinl(th));
       }
     float2* p = nullptr;
     if (cudaMalloc(&p, sizeof(float2) * R) != cudaSuccess) return XFT_ECUDA;
@@ -527,6 +569,10 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
     return XFT_ENOTSUP;
   }
   if (probe) return XFT_OK;
+  if (XFT_RING_PERSIST_MB > 0) {
+    static std::once_flag once;
+    std::call_once(once, []() { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)XFT_RING_PERSIST_MB << 20); });
+  }
   RingPlan pl{};
   pl.R1 = R1;
   pl.R2 = R2;
@@ -565,7 +611,7 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   bf.ticket = reinterpret_cast<unsigned*>(base + ring_bytes + 2 * tab_bytes);
   bf.done1 = bf.ticket + RING_CSTRIDE;
   bf.done2 = bf.done1 + (size_t)pl.nsb * XFT_RING_NSUB * RING_CSTRIDE;
-  int rc = ring_twiddles(LOG1, LOG2, &bf.twr);
+  int rc = ring_twiddles(LOG1, LOG2, Cfg::TR, &bf.twr);
   if (rc) return rc;
   Tables t1, t2;
   if ((rc = get_tables(R1, XFT_C64, &t1, Cfg::E1))) return rc;
@@ -582,7 +628,7 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return XFT_ENOTSUP;
   const int nset = (int)((R > ncounters ? R : ncounters) + 255) / 256;
-  ring_setup_kernel<<<nset, 256, 0, st>>>(pre, post, bf.ticket, ncounters, ck, R1, R2);
+  ring_setup_kernel<<<nset, 256, 0, st>>>(pre, post, bf.ticket, ncounters, ck, R1, R2, Cfg::TR);
   const long long cap = (long long)sms * occ;
   const unsigned grid = (unsigned)(pl.total < cap ? pl.total : cap);
   // cooperative launch: the runtime refuses a grid whose CTAs cannot all be resident, which the
@@ -600,7 +646,7 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   if (cudaLaunchKernelEx(&cfg, kern, map, static_cast<float2*>(out), pl, bf, static_cast<const float2*>(t1.tw),
                          static_cast<const float2*>(t2.tw)) != cudaSuccess) {
     cudaGetLastError();
-    return XFT_ECUDA;
+    return XFT_ENOTSUP;  // e.g. a cooperative grid the device cannot hold right now (MPS/MIG): the caller's other paths
   }
   return XFT_OK;
 }
