@@ -18,7 +18,7 @@ for r in rows[1:]:
     names[r[idi]] = r[ki]
 agg = collections.OrderedDict()
 for i in sorted(per, key=int):
-    n = re.sub(r"\(.*", "", names[i]).replace("void ", "")
+    n = re.sub(r"\(.*", "", names[i].replace("<unnamed>::", "")).replace("void ", "")
     n = re.sub(r"<.*", "", n) + ("<" + ",".join(re.findall(r"(float2|double2|\b\d+\b)", names[i])[:3]) + ">")
     t = per[i].get("gpu__time_duration.sum", (0, ""))
     us = t[0] / 1000.0 if t[1] in ("ns", "nsecond") else (t[0] * 1000 if t[1] in ("ms", "msecond") else t[0])

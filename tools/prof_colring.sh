@@ -9,7 +9,7 @@ ncu --set full --clock-control none --import-source on -k regex:xft_colring_kern
 python tools/ncu_summary.py $T/ring.ncu-rep > $O/summary.txt 2>&1
 python tools/ncu_stalls.py $T/ring.ncu-rep xft_colring_kernel 30 > $O/stalls.txt 2>&1
 python tools/ncu_lines.py $T/ring.ncu-rep xft_colring_kernel > $O/lines.txt 2>&1
-python tools/ncu_opmix.py $T/ring.ncu-rep xft_colring_kernel > $O/opmix.txt 2>&1
+python tools/ncu_opmix.py $T/ring.ncu-rep 40 > $O/opmix.txt 2>&1
 ncu -i $T/ring.ncu-rep --page details > $O/details.txt 2>&1
 rm -f $T/ring.ncu-rep
 ls -la $O
