@@ -193,6 +193,17 @@ int xft_nccl_info(char* path, int path_len, int* version);
 int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, int64_t ld, int dtype,
                     const double* abcd_host, void* workspace, void* stream);
 
+/* Diagnostics (host only, no device work): the tile schedule of the c64 column kernel that
+ * xft_lct_columns / xft_lct2d use for 4096 <= n_rows <= 65536 (two four-step passes through a
+ * scratch ring that stays in L2).  tile (5 ints, may be NULL) = {pass 0|1 (2: past the end),
+ * super-block, column block, line index inside the pass, ring slot} of tile `index`;
+ * info (6 ints, may be NULL) = {tiles, super-blocks, lag, ring slots, tiles per pass-1 and per
+ * pass-2 block-phase}.  A tile may only depend on tiles with a smaller index: pass 2 of a
+ * super-block on all of its pass-1 tiles, pass 1 of super-block s on all pass-2 tiles of
+ * s - slots (the ring slot it overwrites); tests/test_native_cpu.py checks exactly that.
+ * XFT_ENOTSUP for shapes the kernel does not take. */
+int xft_column_schedule(int64_t n_rows, int64_t n_cols, int64_t index, int* tile, int* info);
+
 /* Row LCT (one quadruple, host) written in the all-to-all send layout of the
  * sharded 2-D transform: segment g (2^seg_log2w samples) of row r is stored at
  * out + g*seg_stride + r*2^seg_log2w (seg_stride >= batch * 2^seg_log2w). */

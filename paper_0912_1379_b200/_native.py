@@ -55,6 +55,7 @@ _SIGS = {
     "xft_nccl_info": ([ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "xft_transpose": ([_vp, _vp, _i64, _i64, _i64, _i64, ctypes.c_int, _vp], ctypes.c_int),
     "xft_lct_columns": ([_vp, _vp, _i64, _i64, _i64, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
+    "xft_column_schedule": ([_i64, _i64, _i64, _vp, _vp], ctypes.c_int),
     "xft_lct_rows_packed": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, ctypes.c_int, _i64, _vp], ctypes.c_int),
     "xft_lct_rows_peers": ([_vp, _vp, ctypes.c_int, _i64, _i64, _i64, ctypes.c_int, _vp, _vp], ctypes.c_int),
     "xft_lct_chain": ([_vp, _vp, _i64, _i64, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, _vp],

@@ -521,6 +521,10 @@ int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, i
   return run_lct_cols(in, out, workspace, n_rows, n_cols, ld, dtype, abcd_host, 0, static_cast<cudaStream_t>(stream));
 }
 
+int xft_column_schedule(int64_t n_rows, int64_t n_cols, int64_t index, int* tile, int* info) {
+  return ring_schedule(n_rows, n_cols, index, tile, info);
+}
+
 int xft_lct_rows_packed(const void* in, void* out, int64_t batch, int64_t n, int dtype, const double* abcd_host,
                         int seg_log2w, int64_t seg_stride, void* stream) {
   int rc = xft_validate_lct_params(abcd_host, 1, 0, 1, 1e-10, nullptr);

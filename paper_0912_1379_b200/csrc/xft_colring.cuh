@@ -100,7 +100,7 @@ struct RingTile {
   int sb, cb, idx;
 };
 
-__device__ __forceinline__ RingTile ring_decode(const RingPlan& p, unsigned tk) {
+__host__ __device__ __forceinline__ RingTile ring_decode(const RingPlan& p, unsigned tk) {
   RingTile t;
   if (tk >= p.total) {
     t.phase = 2;
@@ -546,6 +546,32 @@ int ring_twiddles(int l1, int l2, int TR, const float2** out) {
   return XFT_OK;
 }
 
+// the schedule of a [2^(log1+log2)][ncols] column transform with W-column tiles (host side)
+inline RingPlan ring_plan(int log1, int log2, int W, int64_t ncols, int64_t ld, int64_t ld_out) {
+  RingPlan pl{};
+  pl.R1 = 1 << log1;
+  pl.R2 = 1 << log2;
+  pl.nblocks = (int)((ncols + W - 1) / W);
+  pl.SB = XFT_RING_SB;
+  while (pl.nblocks % pl.SB) pl.SB /= 2;
+  pl.nsb = pl.nblocks / pl.SB;
+  pl.lag = pl.nsb < XFT_RING_LAG ? pl.nsb : XFT_RING_LAG;
+  pl.slots = pl.nsb < XFT_RING_SLOTS ? pl.nsb : XFT_RING_SLOTS;
+  pl.T0 = (unsigned)(pl.SB * pl.R2);
+  pl.T1 = (unsigned)(pl.SB * pl.R1);
+  pl.lsb = log2_of(pl.SB);
+  pl.l0 = pl.lsb + log2;
+  pl.l1 = pl.lsb + log1;  // log1 == log2 or log2 + 1: pass-2 block-phases are 1x or 2x the pass-1 ones
+  pl.tA = (unsigned)pl.lag * pl.T0;
+  pl.tB = (unsigned)(pl.nsb - pl.lag) * (pl.T0 + pl.T1);
+  pl.total = pl.tA + pl.tB + (unsigned)pl.lag * pl.T1;
+  if (XFT_RING_ABL & 3) pl.total = (unsigned)pl.nsb * ((XFT_RING_ABL & 1) ? pl.T0 : pl.T1);
+  pl.ld_in = ld;
+  pl.ld_out = ld_out;
+  pl.ncols = (int)ncols;
+  return pl;
+}
+
 template <int LOG1, int LOG2>
 int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t ld_out, const ColChirp& ck,
                    cudaStream_t st, bool probe) {
@@ -573,28 +599,7 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
     static std::once_flag once;
     std::call_once(once, []() { cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)XFT_RING_PERSIST_MB << 20); });
   }
-  RingPlan pl{};
-  pl.R1 = R1;
-  pl.R2 = R2;
-  pl.nblocks = (int)((ncols + W - 1) / W);
-  pl.SB = XFT_RING_SB;
-  while (pl.nblocks % pl.SB) pl.SB /= 2;
-  pl.nsb = pl.nblocks / pl.SB;
-  pl.lag = pl.nsb < XFT_RING_LAG ? pl.nsb : XFT_RING_LAG;
-  pl.slots = pl.nsb < XFT_RING_SLOTS ? pl.nsb : XFT_RING_SLOTS;
-  pl.T0 = (unsigned)(pl.SB * R2);
-  pl.T1 = (unsigned)(pl.SB * R1);
-  pl.lsb = log2_of(pl.SB);
-  pl.l0 = pl.lsb + LOG2;
-  pl.l1 = pl.lsb + LOG1;
-  static_assert(LOG1 == LOG2 || LOG1 == LOG2 + 1, "pass-2 block-phases are 1x or 2x the pass-1 ones");
-  pl.tA = (unsigned)pl.lag * pl.T0;
-  pl.tB = (unsigned)(pl.nsb - pl.lag) * (pl.T0 + pl.T1);
-  pl.total = pl.tA + pl.tB + (unsigned)pl.lag * pl.T1;
-  if (XFT_RING_ABL & 3) pl.total = (unsigned)pl.nsb * ((XFT_RING_ABL & 1) ? pl.T0 : pl.T1);
-  pl.ld_in = ld;
-  pl.ld_out = ld_out;
-  pl.ncols = (int)ncols;
+  const RingPlan pl = ring_plan(LOG1, LOG2, W, ncols, ld, ld_out);
   // scratch: ring, pre/post table rows, counters
   const size_t ring_bytes = (size_t)pl.slots * pl.SB * R * W * sizeof(float2);
   const size_t tab_bytes = (size_t)R * sizeof(float2);
@@ -649,6 +654,15 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
     return XFT_ENOTSUP;  // e.g. a cooperative grid the device cannot hold right now (MPS/MIG): the caller's other paths
   }
   return XFT_OK;
+}
+
+// shape of the K7 tiles for a column height 2^l (12 <= l <= 16): pass lengths and tile width
+inline bool ring_shape(int l, int* log1, int* log2, int* W) {
+  if (l < 12 || l > 16) return false;
+  *log1 = (l + 1) / 2;
+  *log2 = l / 2;
+  *W = *log1 <= 7 ? XFT_RING_W : XFT_RING_W / 4;
+  return true;
 }
 
 // c64 columns of height 2^12 .. 2^16 (R1 x R2 = 64x64 .. 256x256); anything else: XFT_ENOTSUP, nothing launched

@@ -57,6 +57,8 @@ int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, 
                  const double* abcd_host, int flags, cudaStream_t st);
 // true when run_lct_cols takes the L2-staged one-round-trip path (K7, xft_colring.cuh) for this shape
 bool lct_cols_ring_ok(const void* in, int64_t R, int64_t ncols, int64_t ld, int dtype);
+// the K7 tile schedule, host side (xft_column_schedule)
+int ring_schedule(int64_t R, int64_t ncols, int64_t index, int* out, int* info);
 // the cluster (one HBM round trip) column kernel alone, with a separate output row stride;
 // probe = true checks that the kernel can run this shape on this device (cluster
 // occupancy, tensor-map encoding) and launches nothing

@@ -1547,6 +1547,33 @@ bool lct_cols_ring_ok(const void* in, int64_t R, int64_t ncols, int64_t ld, int 
   return lct_cols_ring(in, nullptr, R, ncols, ld, ld, k, nullptr, true) == XFT_OK;
 }
 
+// K7 schedule of tile `index` (host only): out = {pass, super-block, column block, line index, ring slot},
+// info = {tiles, super-blocks, lag, slots, tiles per pass-1 / pass-2 block-phase}
+int ring_schedule(int64_t R, int64_t ncols, int64_t index, int* out, int* info) {
+  const int l = log2_of(R);
+  int l1, l2, W;
+  if ((int64_t(1) << l) != R || ncols < 1 || !ring_shape(l, &l1, &l2, &W)) return XFT_ENOTSUP;
+  const RingPlan pl = ring_plan(l1, l2, W, ncols, ncols, ncols);
+  if (info) {
+    info[0] = (int)pl.total;
+    info[1] = pl.nsb;
+    info[2] = pl.lag;
+    info[3] = pl.slots;
+    info[4] = (int)pl.T0;
+    info[5] = (int)pl.T1;
+  }
+  if (out) {
+    if (index < 0) return XFT_EINVALID_SIZE;
+    const RingTile t = ring_decode(pl, (unsigned)(index < (int64_t)pl.total ? index : pl.total));
+    out[0] = t.phase;
+    out[1] = t.sb;
+    out[2] = t.cb;
+    out[3] = t.idx;
+    out[4] = t.phase == 2 ? -1 : t.sb % pl.slots;
+  }
+  return XFT_OK;
+}
+
 int run_lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int64_t ld, int dtype,
                  const double* abcd_host, int flags, cudaStream_t st) {
   const int l = log2_of(R);

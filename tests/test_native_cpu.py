@@ -111,3 +111,51 @@ def test_no_cuda_means_loud_failure(monkeypatch):
         pytest.skip("GPU present")
     with pytest.raises(_native.NativeUnavailable):
         X.fast_lct(X.LctParams.fourier(), X.Signal(X.asymptotic_zeros(8), np.ones(8)))
+
+
+@pytest.mark.parametrize("R,ncols", [(16384, 16384), (16384, 24), (4096, 64), (4096, 2048), (8192, 528), (32768, 40),
+                                     (65536, 200), (16384, 64 * 7)])
+def test_column_ring_schedule_is_deadlock_free(R, ncols):
+    """The tile order of the L2-staged column kernel (xft_colring.cuh): every (pass, block, line) once,
+    and each tile's dependencies carry smaller indices -- pass 2 of a super-block after all of its
+    pass-1 tiles, pass 1 of super-block s after every pass-2 tile of s - slots (the ring slot it
+    overwrites).  With CTA b running tiles b, b + grid, ... in order on a cooperative (all-resident)
+    grid, the lowest unfinished tile can then always run."""
+    lib = _lib_or_skip()
+    info = (ctypes.c_int * 6)()
+    tile = (ctypes.c_int * 5)()
+    assert lib.xft_column_schedule(R, ncols, 0, tile, info) == 0
+    total, nsb, lag, slots, t0, t1 = list(info)
+    assert 1 <= lag <= nsb and 1 <= slots <= nsb and total == nsb * (t0 + t1)
+    seen = set()
+    last_p1 = {}   # super-block -> largest pass-1 index
+    first_p2 = {}  # super-block -> smallest pass-2 index
+    last_p2 = {}
+    first_p1 = {}
+    count = {}
+    for i in range(total):  # every tile: the decode is host code, microseconds each
+        assert lib.xft_column_schedule(R, ncols, i, tile, None) == 0
+        ph, sb, cb, idx, slot = list(tile)
+        assert ph in (0, 1) and 0 <= sb < nsb and slot == sb % slots
+        key = (ph, cb, idx)
+        assert key not in seen
+        seen.add(key)
+        count[(ph, sb)] = count.get((ph, sb), 0) + 1
+        if ph == 0:
+            last_p1[sb] = i
+            first_p1.setdefault(sb, i)
+        else:
+            first_p2.setdefault(sb, i)
+            last_p2[sb] = i
+    assert lib.xft_column_schedule(R, ncols, total, tile, None) == 0 and tile[0] == 2
+    for sb in range(nsb):
+        assert count[(0, sb)] == t0 and count[(1, sb)] == t1
+        assert last_p1[sb] < first_p2[sb]
+        if sb >= slots:
+            assert last_p2[sb - slots] < first_p1[sb]
+
+
+def test_column_ring_schedule_rejects_other_shapes():
+    lib = _lib_or_skip()
+    for R, nc in ((2048, 64), (1 << 17, 64), (5000, 64), (16384, 0)):
+        assert lib.xft_column_schedule(R, nc, 0, None, None) != 0
