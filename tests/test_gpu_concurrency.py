@@ -214,3 +214,29 @@ def test_host_path_from_two_threads_matches_device_path():
     got = _run_threads([lambda: ops.lct_host(a.values, a.abcd), lambda: ops.lct_host(b.values, b.abcd)])
     assert np.array_equal(got[0], ops.lct_rows(torch.from_numpy(a.values).cuda(), a.abcd).cpu().numpy())
     assert np.array_equal(got[1], ops.lct_rows(torch.from_numpy(b.values).cuda(), b.abcd).cpu().numpy())
+
+
+def test_lct2d_from_four_threads_matches_serial():
+    """The 2-D transform's L2-staged column kernel (K7) launched from four threads at once, each on
+    its own stream: every launch is a cooperative, GPU-filling persistent grid with its own scratch
+    ring and counters (per-stream scratch), so concurrent calls must queue, not interfere."""
+    from paper_0912_1379_b200 import lct2d
+
+    rng = np.random.default_rng(77)
+    p = (1.0, 0.25, 0.0, 1.0)
+    fields = [torch.from_numpy((rng.normal(size=(4096, 512)) + 1j * rng.normal(size=(4096, 512))).astype(np.complex64)).cuda()
+              for _ in range(4)]
+    serial = [lct2d.lct2d(f, p, p).cpu().numpy() for f in fields]
+    torch.cuda.synchronize()
+
+    def job(f):
+        def run():
+            out = None
+            for _ in range(3):
+                out = lct2d.lct2d(f, p, p)
+            return out.cpu().numpy()
+        return run
+
+    got = _run_threads([job(f) for f in fields])
+    for g, s in zip(got, serial):
+        assert np.array_equal(g, s)
