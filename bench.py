@@ -618,7 +618,7 @@ def roofline_of(name, rec, world, peak, peak_src, fp64_peak):
     dom = max(per, key=lambda t: per[t]["kernel_ms"])
     kind = work[[it.tag for it in work].index(dom)].kind
     kname = {"lct": "xft_pipe_kernel", "mehler": "xft_blue_kernel + xft_tile_kernel",
-             "lct2d": "xft_pipe_kernel + xft_colclu_kernel"}[kind]
+             "lct2d": "xft_pipe_kernel + xft_colring_kernel"}[kind]
     roof = {"bound": "hbm", "achieved": per[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
             "frac": per[dom]["frac"], "traffic": per[dom]["traffic"], "kernel": f"{kname} {dom}",
             "peak_source": peak_src,

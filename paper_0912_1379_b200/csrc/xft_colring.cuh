@@ -6,7 +6,7 @@
 // j = k1 + R1 k2.  Run as two kernels the [R][ncols] intermediate crosses HBM
 // twice more.  Here ONE persistent kernel runs both passes over a stream of
 // W-column "blocks" (W = 64: 512-byte row segments): the pass-1 tiles of a
-// block write one slot of a small ring of scratch (6 slots x 8 MB at R = 16384:
+// block write one slot of a small ring of scratch (5 slots x 8 MB at R = 16384:
 // it lives in the 126 MB L2), and the pass-2 tiles of the same block follow a
 // few blocks later, once every pass-1 tile of the block has signalled
 // (per-block completion counters, release/acquire at GPU scope).  The slot is
@@ -43,10 +43,10 @@
 #define XFT_RING_SB 1      // column blocks per super-block (the unit of the ring and of the counters)
 #endif
 #ifndef XFT_RING_LAG
-#define XFT_RING_LAG 3     // super-blocks between a block's pass 1 and its pass 2
+#define XFT_RING_LAG 2     // super-blocks between a block's pass 1 and its pass 2
 #endif
 #ifndef XFT_RING_SLOTS
-#define XFT_RING_SLOTS 6   // ring slots (super-blocks of scratch)
+#define XFT_RING_SLOTS 5   // ring slots (super-blocks of scratch)
 #endif
 #ifndef XFT_RING_STAGES
 #define XFT_RING_STAGES 3  // TMA stages per CTA

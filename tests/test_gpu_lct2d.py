@@ -45,9 +45,9 @@ def test_lct2d_vs_oracle(torch, L2, shape, dtype, tol):
     assert rel_l2(got, ref) <= tol
 
 
-def test_packed_rows_and_columns_emulate_shards(torch, L2):
+@pytest.mark.parametrize("n,G", [(1024, 4), (4096, 4)])  # 4096: the slabs' columns take the L2-staged path (K7)
+def test_packed_rows_and_columns_emulate_shards(torch, L2, n, G):
     """G virtual shards on one GPU: packed row pass per shard, the all-to-all as a copy, column pass per slab."""
-    n, G = 1024, 4
     rng = np.random.default_rng(9)
     f = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(np.complex64)
     ft = torch.from_numpy(f).cuda()
