@@ -194,7 +194,7 @@ int xft_lct_columns(const void* in, void* out, int64_t n_rows, int64_t n_cols, i
                     const double* abcd_host, void* workspace, void* stream);
 
 /* Diagnostics (host only, no device work): the tile schedule of the c64 column kernel that
- * xft_lct_columns / xft_lct2d use for 4096 <= n_rows <= 65536 (two four-step passes through a
+ * xft_lct_columns / xft_lct2d use for 16384 <= n_rows <= 65536 (two four-step passes through a
  * scratch ring that stays in L2).  tile (5 ints, may be NULL) = {pass 0|1 (2: past the end),
  * super-block, column block, line index inside the pass, ring slot} of tile `index`;
  * info (6 ints, may be NULL) = {tiles, super-blocks, lag, ring slots, tiles per pass-1 and per

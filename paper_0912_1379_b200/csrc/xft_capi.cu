@@ -455,7 +455,7 @@ int xft_lct2d(const void* in, void* out, int64_t n_rows, int64_t n_cols, int dty
   const int lr = log2_exact(n_rows), lc = log2_exact(n_cols);
   const int64_t nc = n_cols / 8;
   // (only where the cluster column kernel runs on this device: probed first, nothing launched)
-  // (c64 fields 4096 .. 65536 rows high skip this: their columns run in place through the L2-staged path)
+  // (c64 fields 16384 .. 65536 rows high skip this: their columns run in place through the L2-staged path)
   if (workspace && XFT_LCT2D_SLABS && !lct_cols_ring_ok(out, n_rows, n_cols, n_cols, dtype) && lr >= 11 && lr <= 14 && lc >= 0 && lc <= (dtype == XFT_C64 ? MAXLOG_C64 : MAXLOG_C128) &&
       nc >= 256 && nc % 8 == 0 &&
       run_lct_cols_cluster(workspace, out, n_rows, nc, nc, n_cols, dtype, abcd_col, 0, st, true) == XFT_OK) {

@@ -656,22 +656,22 @@ int launch_colring(const void* in, void* out, int64_t ncols, int64_t ld, int64_t
   return XFT_OK;
 }
 
-// shape of the K7 tiles for a column height 2^l (12 <= l <= 16): pass lengths and tile width
+// shape of the K7 tiles for a column height 2^l (14 <= l <= 16): pass lengths and tile width
 inline bool ring_shape(int l, int* log1, int* log2, int* W) {
-  if (l < 12 || l > 16) return false;
+  if (l < 14 || l > 16) return false;
   *log1 = (l + 1) / 2;
   *log2 = l / 2;
   *W = *log1 <= 7 ? XFT_RING_W : XFT_RING_W / 4;
   return true;
 }
 
-// c64 columns of height 2^12 .. 2^16 (R1 x R2 = 64x64 .. 256x256); anything else: XFT_ENOTSUP, nothing launched
+// c64 columns of height 2^14 .. 2^16 (R1 x R2 = 128x128 .. 256x256); anything else: XFT_ENOTSUP, nothing launched.
+// (Measured on 4096- and 8192-row fields the cluster kernel K6 is faster -- 0.10 vs 0.15 ms at 4096^2, 0.39 vs
+// 0.43 ms at 8192^2: shorter passes leave less work per tile handshake -- so those heights stay with K6.)
 inline int lct_cols_ring(const void* in, void* out, int64_t R, int64_t ncols, int64_t ld, int64_t ld_out,
                          const ColChirp& ck, cudaStream_t st, bool probe = false) {
   if (!XFT_COLRING) return XFT_ENOTSUP;
   switch (log2_of(R)) {
-    case 12: return launch_colring<6, 6>(in, out, ncols, ld, ld_out, ck, st, probe);
-    case 13: return launch_colring<7, 6>(in, out, ncols, ld, ld_out, ck, st, probe);
     case 14: return launch_colring<7, 7>(in, out, ncols, ld, ld_out, ck, st, probe);
     case 15: return launch_colring<8, 7>(in, out, ncols, ld, ld_out, ck, st, probe);
     case 16: return launch_colring<8, 8>(in, out, ncols, ld, ld_out, ck, st, probe);

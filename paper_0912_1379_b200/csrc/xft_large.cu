@@ -1484,7 +1484,7 @@ int lct_cols(const void* in, void* out, void* ws, int64_t R, int64_t ncols, int6
     const double2 *ptab = nullptr, *cptab = nullptr;
     int rc = boundary_tables(R, &ptab, &cptab);
     if (rc) return rc;
-    if constexpr (sizeof(C) == 8) {  // c64, 2^12 .. 2^16 rows: two passes through an L2-resident ring (K7)
+    if constexpr (sizeof(C) == 8) {  // c64, 2^14 .. 2^16 rows: two passes through an L2-resident ring (K7)
       rc = lct_cols_ring(in, out, R, ncols, ld, ld, k, st);
       if (rc != XFT_ENOTSUP) return rc;
     }

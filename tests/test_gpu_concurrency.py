@@ -224,7 +224,7 @@ def test_lct2d_from_four_threads_matches_serial():
 
     rng = np.random.default_rng(77)
     p = (1.0, 0.25, 0.0, 1.0)
-    fields = [torch.from_numpy((rng.normal(size=(4096, 512)) + 1j * rng.normal(size=(4096, 512))).astype(np.complex64)).cuda()
+    fields = [torch.from_numpy((rng.normal(size=(16384, 256)) + 1j * rng.normal(size=(16384, 256))).astype(np.complex64)).cuda()
               for _ in range(4)]
     serial = [lct2d.lct2d(f, p, p).cpu().numpy() for f in fields]
     torch.cuda.synchronize()

@@ -34,8 +34,10 @@ ABCD5 = (1.0, 0.25, 0.0, 1.0)
                                              ((100, 48), np.complex128, 1e-12),
                                              # slab route (row pass into 8 column slabs, cluster columns)
                                              ((2048, 2048), np.complex128, 1e-12), ((4096, 2048), np.complex64, 2e-5),
-                                             # L2-staged columns (K7): several super-blocks, ring slots reused
-                                             ((4096, 1024), np.complex64, 2e-5), ((8192, 528), np.complex64, 2e-5)])
+                                             ((4096, 1024), np.complex64, 2e-5), ((8192, 528), np.complex64, 2e-5),
+                                             # L2-staged columns (K7): several super-blocks, ring slots reused,
+                                             # a ragged last block
+                                             ((16384, 528), np.complex64, 2e-5)])
 def test_lct2d_vs_oracle(torch, L2, shape, dtype, tol):
     rng = np.random.default_rng(5)
     f = (rng.normal(size=shape) + 1j * rng.normal(size=shape)).astype(dtype)
@@ -45,7 +47,7 @@ def test_lct2d_vs_oracle(torch, L2, shape, dtype, tol):
     assert rel_l2(got, ref) <= tol
 
 
-@pytest.mark.parametrize("n,G", [(1024, 4), (4096, 4)])  # 4096: the slabs' columns take the L2-staged path (K7)
+@pytest.mark.parametrize("n,G", [(1024, 4), (4096, 4)])
 def test_packed_rows_and_columns_emulate_shards(torch, L2, n, G):
     """G virtual shards on one GPU: packed row pass per shard, the all-to-all as a copy, column pass per slab."""
     rng = np.random.default_rng(9)

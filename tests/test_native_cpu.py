@@ -113,7 +113,7 @@ def test_no_cuda_means_loud_failure(monkeypatch):
         X.fast_lct(X.LctParams.fourier(), X.Signal(X.asymptotic_zeros(8), np.ones(8)))
 
 
-@pytest.mark.parametrize("R,ncols", [(16384, 16384), (16384, 24), (4096, 64), (4096, 2048), (8192, 528), (32768, 40),
+@pytest.mark.parametrize("R,ncols", [(16384, 16384), (16384, 24), (16384, 2048), (32768, 528), (32768, 40),
                                      (65536, 200), (16384, 64 * 7)])
 def test_column_ring_schedule_is_deadlock_free(R, ncols):
     """The tile order of the L2-staged column kernel (xft_colring.cuh): every (pass, block, line) once,
@@ -157,5 +157,5 @@ def test_column_ring_schedule_is_deadlock_free(R, ncols):
 
 def test_column_ring_schedule_rejects_other_shapes():
     lib = _lib_or_skip()
-    for R, nc in ((2048, 64), (1 << 17, 64), (5000, 64), (16384, 0)):
+    for R, nc in ((2048, 64), (8192, 64), (1 << 17, 64), (20000, 64), (16384, 0)):
         assert lib.xft_column_schedule(R, nc, 0, None, None) != 0
