@@ -284,3 +284,36 @@ def test_config5_256_rows_and_256_columns_independent(torch, L2):
     for i, c in enumerate(idx):
         assert rel_l2(out[:, c], want_cols[i]) <= 2e-5, ("column", c)
         assert rel_l2(out[c, :], want_rows[i]) <= 2e-5, ("row", c)
+
+
+@pytest.mark.parametrize("nc,ld", [(64, 64), (65, 66), (200, 256), (1000, 1024)])
+def test_ring_columns_ragged_and_repeatable(torch, L2, nc, ld):
+    """The L2-staged column kernel (16384 rows, c64) on ragged slabs: partial last 64-column block, row
+    stride > width.  In place == out of place bit for bit, repeated runs identical (the schedule has no
+    data-dependent order), columns beyond the slab untouched, sampled columns against the oracle."""
+    from paper_0912_1379_b200 import _native, ops
+
+    R = 16384
+    rng = np.random.default_rng(nc)
+    full = (rng.normal(size=(R, ld)) + 1j * rng.normal(size=(R, ld))).astype(np.complex64)
+    p = np.array((0.5, 1.5, -0.5, 0.5))
+    src = torch.from_numpy(full).cuda()
+    ws = torch.empty_like(src)
+
+    def run(dst):
+        _native.call("xft_lct_columns", src.data_ptr() if dst is not src else dst.data_ptr(), dst.data_ptr(), R, nc, ld,
+                     ops._dtype_code(src), p.ctypes.data, ws.data_ptr(), ops._stream_ptr(src.device))
+        return dst.cpu().numpy()
+
+    a = run(torch.full_like(src, 7.0))
+    b = run(torch.full_like(src, 7.0))
+    assert np.array_equal(a, b)
+    if ld > nc:
+        assert np.all(a[:, nc:] == 7.0)
+    c = run(src)  # in place (src is overwritten: last)
+    assert np.array_equal(c[:, :nc], a[:, :nc])
+    if ld > nc:
+        assert np.array_equal(c[:, nc:], full[:, nc:])
+    for col in sorted({0, nc // 2, nc - 1}):
+        _, ref = O.fast_lct_rows(tuple(p), full[:, col].astype(complex))
+        assert rel_l2(a[:, col], ref) <= 2e-5
