@@ -82,6 +82,9 @@
 #ifndef XFT_RING_PERSIST_MB
 #define XFT_RING_PERSIST_MB 0  // > 0: set the device's persisting-L2 set-aside once (48: the ring stops leaking to HBM,
 #endif                         // 2.9 -> 2.1 GB written, but the kernel slows 1.26 -> 1.40 ms: less L2 for the streams)
+#ifndef XFT_RING_XBAR
+#define XFT_RING_XBAR 0    // 1: the "tile has been read" barrier of the compute warps is a split mbarrier phase
+#endif
 #ifndef XFT_RING_HINT
 #define XFT_RING_HINT 1    // L2 eviction hints: input evict_first, scratch evict_last
 #endif
@@ -208,8 +211,10 @@ struct RingCfg {
   static constexpr int W = LMAXR <= 128 ? XFT_RING_W : XFT_RING_W / 4, TR = XFT_RING_TR, THREADS = W * TR;
   static constexpr int MINB = LMAXR <= 128 ? XFT_RING_MINB : (XFT_RING_W >= 64 ? 2 : 1);
   static constexpr int E1 = R1 / TR, E2 = R2 / TR;
-  using Fft1 = PipeCfg<C, LOG1, E1, MODE_DFT, -1, W, 1, 1, 0, THREADS>;  // exchange barriers: the compute warps only
-  using Fft2 = PipeCfg<C, LOG2, E2, MODE_DFT, -1, W, 1, 1, 0, THREADS>;
+  // exchange barriers: the compute warps only; XFT_RING_XBAR: "tile read" is an mbarrier phase (PipeCfg::XBAR)
+  using Fft1 = PipeCfg<C, LOG1, E1, MODE_DFT, -1, W, 1, 1, 0, THREADS, XFT_RING_XBAR>;
+  using Fft2 = PipeCfg<C, LOG2, E2, MODE_DFT, -1, W, 1, 1, 0, THREADS, XFT_RING_XBAR>;
+  static constexpr int XB = Fft1::NPASS > Fft2::NPASS ? Fft1::NPASS : Fft2::NPASS;  // split barriers per stage
   static constexpr int NPMAX = LMAXR + LMAXR / 16;
   static constexpr int LS = NPMAX + (((1 - NPMAX % 16) % 16) + 16) % 16;  // == 1 (mod 16): W lines x 1 slot per wavefront
   // stages; completion barriers (tiles whose stores may still be unsignalled); tile-info slots
@@ -310,6 +315,7 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
   __shared__ __align__(8) uint64_t done[ND];
+  __shared__ __align__(8) uint64_t rdbar[NS][Cfg::XB];  // XFT_RING_XBAR: the stage's tile / exchanges have been read
   __shared__ RingTile info[NI];
   __shared__ volatile int nsig;  // sequences signalled so far (signaller -> issuer)
   C* const stages = reinterpret_cast<C*>(xft_smem);
@@ -324,6 +330,7 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], Cfg::THREADS);
+      for (int x = 0; x < Cfg::XB; ++x) mbar_init(&rdbar[s][x], Cfg::THREADS / 32);
     }
 #pragma unroll
     for (int s = 0; s < ND; ++s) mbar_init(&done[s], Cfg::THREADS);
@@ -444,6 +451,7 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
     }
     C* const S = stages + st * Cfg::STAGE;
     const int col = ti.cb * W + w;
+    const XBar xb{rdbar[st], i / NS};
     if (ti.phase == 0) {
       constexpr int E = Cfg::E1;
       C v[E], tq[E];
@@ -466,7 +474,12 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
           tq[s + 1] = make_float2(q.z, q.w);
         }
       }
-      if (!(XFT_RING_ABL & 4)) pipe_passes<typename Cfg::Fft1, 0>(v, S + w * Cfg::LS, j, tw1, noop);
+      if constexpr (Cfg::Fft1::XBAR) {
+        xb.template arrive<0>();  // this warp has read its part of the tile and of the table rows
+        pipe_passes_x<typename Cfg::Fft1, 0>(v, S + w * Cfg::LS, j, tw1, noop, xb);
+      } else if (!(XFT_RING_ABL & 4)) {
+        pipe_passes<typename Cfg::Fft1, 0>(v, S + w * Cfg::LS, j, tw1, noop);
+      }
       mbar_arrive(&empty[st]);  // this thread is done with the stage
       C* dst = slot_base(ti) + (long long)ti.idx * W + w;
 #pragma unroll
@@ -496,7 +509,12 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
           pq[s + 1] = make_float2(p.z, p.w);
         }
       }
-      if (!(XFT_RING_ABL & 4)) pipe_passes<typename Cfg::Fft2, 0>(v, S + w * Cfg::LS, j, tw2, noop);
+      if constexpr (Cfg::Fft2::XBAR) {
+        xb.template arrive<0>();
+        pipe_passes_x<typename Cfg::Fft2, 0>(v, S + w * Cfg::LS, j, tw2, noop, xb);
+      } else if (!(XFT_RING_ABL & 4)) {
+        pipe_passes<typename Cfg::Fft2, 0>(v, S + w * Cfg::LS, j, tw2, noop);
+      }
       mbar_arrive(&empty[st]);
       if (col < pl.ncols) {
         C* dst = out + (long long)ti.idx * pl.ld_out + col;

@@ -88,6 +88,20 @@
 #define XFT_SPLIT2 0  // 1: also at two single-row CTAs per SM (c128 n = 4096, the spare ~36 KB per CTA): A/B 121.0 vs 119.2 us, off
 #endif
 
+// Split "buffer read" barriers (PipeCfg::XBAR).  A/B on one box (outputs bit-identical): the 512-thread,
+// one-CTA-per-SM c64 row kernel (n = 16384) 1016 -> 951 us; with 2 or 4 CTAs per SM, where the other CTAs already
+// fill a CTA-wide rendezvous, it LOSES: config 2 c64 52.8 -> 58.3 us, c128 117.4 -> 126.5 us (n = 8192: 296 ->
+// 335 us), config 4 184.9 -> 188.2 us.  Hence: c64 at one CTA per SM only.
+#ifndef XFT_XBAR64
+#define XFT_XBAR64 1      // c64 row kernels at one CTA per SM
+#endif
+#ifndef XFT_XBAR64_ALL
+#define XFT_XBAR64_ALL 0  // every c64 row kernel
+#endif
+#ifndef XFT_XBAR128
+#define XFT_XBAR128 0     // c128 row kernels
+#endif
+
 #ifndef XFT_SKELETON
 #define XFT_SKELETON 0  // tuning only: 1 = exchanges without math, 2 = pure copy
 #endif
@@ -438,7 +452,7 @@ using ChirpTurnWalk = std::conditional_t<XFT_WALK32 != 0, TurnWalk32, TurnWalk>;
 // configuration
 // ---------------------------------------------------------------------------
 template <class C_, int LOG2N_, int E_, int MODE_, int SIGN_, int ROWS_, int STAGES_, int MINB_, int SPLITOK_ = 0,
-          int BARTH_ = 0>
+          int BARTH_ = 0, int XBAR_ = -1>
 struct PipeCfg {
   // threads that take part in the exchange barriers: 0 = the whole CTA (__syncthreads), else a named
   // barrier over the first BARTH threads (kernels with extra, non-computing warps)
@@ -486,6 +500,19 @@ struct PipeCfg {
   static constexpr bool TWBASE = SPLITOK_ && C128 && MODE == MODE_LCT && XFT_TWBASE && XFT_TWGEN && E == 16 &&
                                  NPASS <= E && MINB_ == 1;
   static constexpr size_t SMEM = MAIN + size_t(SPLIT) * sizeof(C);
+  // Split exchange barriers (row kernels): "every thread has finished reading the buffer" is an
+  // mbarrier phase -- each warp arrives right after its reads and only waits just before its next
+  // exchange stores, one butterfly pass later -- instead of a CTA-wide rendezvous in front of the
+  // stores; the barrier between the stores and the loads stays.  With one stage the last phase of a
+  // row (last exchange read) is waited for by thread 0 alone, which then issues the next row's load.
+  // XBAR_: -1 = the row kernels' choice (XFT_XBAR* above), 0 = off, 1 = on for a caller that brings its own
+  // mbarriers and does not need the last exchange's phase (the column ring kernel: its `empty` barrier)
+  static constexpr bool XBAR =
+      XFT_SKELETON == 0 && THREADS % 32 == 0 &&
+      (XBAR_ >= 0 ? XBAR_ != 0
+                  : SPLITOK_ && BARTH_ == 0 &&
+                        (sizeof(C_) == 16 ? XFT_XBAR128 != 0 : (XFT_XBAR64_ALL || (XFT_XBAR64 && MINB_ == 1))));
+  static constexpr bool XBAR_LAST = XBAR && XBAR_ < 0 && STAGES_ == 1;
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
   static_assert(THREADS <= 1024, "threads");
@@ -531,10 +558,32 @@ __device__ __forceinline__ void pipe_sync() {
   else __syncthreads();
 }
 
+// split-barrier handle of a thread: NPASS mbarriers (one arrival per warp each), barrier IDX used once per row --
+// IDX = 0: the input tile has been read, IDX = p: exchange p - 1 has been read -- so the phase parity is the row
+// iteration's and no per-thread phase counter is carried (registers: the c128 CTAs run at their 128-register cap)
+struct XBar {
+  uint64_t* bars = nullptr;
+  int it = 0;
+  template <int IDX>
+  __device__ __forceinline__ void arrive() const {  // this warp has finished reading the buffer
+    __syncwarp();
+    // one elected lane arrives for the warp (elect.sync: no lane index held in a register)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n"
+        "}\n" ::"r"(smem_addr(bars + IDX))
+        : "memory");
+  }
+  template <int IDX>
+  __device__ __forceinline__ void wait() const { mbar_wait(bars + IDX, (uint32_t)it & 1u); }
+};
+
 template <class Cfg, int P, bool FREE_EARLY, class Release, class Free>
 __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
                                           const typename Cfg::C* __restrict__ tw, Release&& release,
-                                          Free&& free_hook, typename Cfg::C (&wpre)[Cfg::E]) {
+                                          Free&& free_hook, typename Cfg::C (&wpre)[Cfg::E], const XBar& xb) {
   using C = typename Cfg::C;
   constexpr int E = Cfg::E, TR = Cfg::TR;
   constexpr int R = (P == 0) ? Cfg::R0 : E;
@@ -642,7 +691,9 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     for (int t = 0; t < R; ++t) v[b + t * NB] = u[t];
   }
   if constexpr (!LAST) {
-    pipe_sync<Cfg>();  // every thread is done reading this buffer
+    // every thread is done reading this buffer
+    if constexpr (Cfg::XBAR) xb.template wait<P>();  // (arrivals: after the pre-multiply reads / the previous exchange's loads)
+    else pipe_sync<Cfg>();
     if constexpr (P == 0) release();  // (first-barrier hook)
     // Stockham store: element t of butterfly i goes to base + t NS, base =
     // (i - k) R + k.  (base mod 16) + (t NS mod 16) < 16 for every thread (NS
@@ -671,7 +722,15 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
     const C* src = rs + pad_idx(j);
 #pragma unroll
     for (int s = 0; s < E; ++s) v[s] = src[s * TR + ((s * TR) >> 4)];
-    if constexpr (FREE_EARLY && P == Cfg::NPASS - 2) {
+    if constexpr (Cfg::XBAR) {
+      // the last exchange's phase is only needed (and only waited for, by thread 0) where the
+      // buffer is handed back to the TMA right away: single-stage CTAs
+      if constexpr (P < Cfg::NPASS - 2 || Cfg::XBAR_LAST) xb.template arrive<P + 1>();
+      if constexpr (FREE_EARLY && P == Cfg::NPASS - 2) {
+        if (threadIdx.x == 0) xb.template wait<P + 1>();
+        free_hook();
+      }
+    } else if constexpr (FREE_EARLY && P == Cfg::NPASS - 2) {
       pipe_sync<Cfg>();
       free_hook();
     }
@@ -681,10 +740,10 @@ __device__ __forceinline__ void pipe_pass(typename Cfg::C (&v)[Cfg::E], typename
 template <class Cfg, int P, bool FREE_EARLY, class Release, class Free>
 __device__ __forceinline__ void pipe_passes_w(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
                                               const typename Cfg::C* __restrict__ tw, Release&& release,
-                                              Free&& free_hook, typename Cfg::C (&wpre)[Cfg::E]) {
+                                              Free&& free_hook, typename Cfg::C (&wpre)[Cfg::E], const XBar& xb) {
   if constexpr (P < Cfg::NPASS) {
-    pipe_pass<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre);
-    pipe_passes_w<Cfg, P + 1, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre);
+    pipe_pass<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre, xb);
+    pipe_passes_w<Cfg, P + 1, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre, xb);
   }
 }
 
@@ -693,13 +752,24 @@ __device__ __forceinline__ void pipe_passes(typename Cfg::C (&v)[Cfg::E], typena
                                             const typename Cfg::C* __restrict__ tw, Release&& release,
                                             Free&& free_hook) {
   typename Cfg::C wpre[Cfg::E];
-  pipe_passes_w<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre);
+  XBar none;  // (callers of this overload never set Cfg::XBAR)
+  static_assert(!Cfg::XBAR, "split barriers need the caller's mbarriers");
+  pipe_passes_w<Cfg, P, FREE_EARLY>(v, rs, j, tw, release, free_hook, wpre, none);
 }
 
 template <class Cfg, int P, class Release>
 __device__ __forceinline__ void pipe_passes(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
                                             const typename Cfg::C* __restrict__ tw, Release&& release) {
   pipe_passes<Cfg, P, false>(v, rs, j, tw, release, []() {});
+}
+
+// the same with the caller's split barriers (Cfg::XBAR; the caller has arrived on barrier 0 after its own reads)
+template <class Cfg, int P, class Release>
+__device__ __forceinline__ void pipe_passes_x(typename Cfg::C (&v)[Cfg::E], typename Cfg::C* rs, int j,
+                                              const typename Cfg::C* __restrict__ tw, Release&& release,
+                                              const XBar& xb) {
+  typename Cfg::C wpre[Cfg::E];
+  pipe_passes_w<Cfg, P, false>(v, rs, j, tw, release, []() {}, wpre, xb);
 }
 
 // ---------------------------------------------------------------------------
@@ -1034,6 +1104,7 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   constexpr int N = Cfg::N, ROWS = Cfg::ROWS, S = Cfg::STAGES;
   extern __shared__ __align__(128) unsigned char xft_smem[];
   __shared__ __align__(8) uint64_t bars[S];
+  __shared__ __align__(8) uint64_t xbars[Cfg::NPASS];  // PipeCfg::XBAR: the "buffer read" phases, one arrival per warp
   // per-row coefficients of the next CH tiles of this CTA, computed by all
   // threads together once per CH tiles (one make_coef latency per chunk)
   constexpr int CH = Cfg::MODE == MODE_LCT ? (Cfg::C128 && ROWS == 1 ? XFT_C128_CH
@@ -1099,6 +1170,8 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
   }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], SPLIT ? 2 : 1);  // split: one arrival per part
+    if constexpr (Cfg::XBAR)
+      for (int s = 0; s < Cfg::NPASS; ++s) mbar_init(&xbars[s], Cfg::THREADS / 32);
     fence_mbar_init();
   }
   if constexpr (Cfg::C128) {
@@ -1175,6 +1248,8 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
     } else {
       pre_multiply<Cfg>(v, rs, j, rc, tc, kc, ptab, tab);
     }
+    const XBar xb{xbars, it};
+    if constexpr (Cfg::XBAR) xb.template arrive<0>();  // this warp has read its share of the input tile
     // the reference rejects non-finite samples (xft/lct.py:125-126): when the
     // caller asks (kc.bad), the pre-multiplied samples are checked right here --
     // a unit-modulus pre-multiplier keeps Inf/NaN non-finite -- two integer ops
@@ -1211,10 +1286,14 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
       first_barrier();
       if constexpr (EARLY) stage_free();  // (the passes that would free the stage are skipped)
     } else {
-      pipe_passes_w<Cfg, 0, EARLY>(v, xs, j, tw, first_barrier, stage_free, wbase);
+      pipe_passes_w<Cfg, 0, EARLY>(v, xs, j, tw, first_barrier, stage_free, wbase, xb);
     }
     if constexpr (S == 1 && !EARLY) {
-      __syncthreads();
+      if constexpr (Cfg::XBAR) {  // thread 0 alone waits for the last exchange's reads
+        if (tid == 0) xb.template wait<Cfg::NPASS - 1>();
+      } else {
+        __syncthreads();
+      }
       stage_free();
     }
 

@@ -30,9 +30,15 @@ def t(fn, reps=10):
     return e0.elapsed_time(e1) / reps
 
 
+torch.manual_seed(7)
 f = torch.randn(n, n, dtype=torch.complex64, device="cuda")
 full = f.clone()
 ws = torch.empty_like(full)
 out = torch.empty_like(full)
 print(f"{tag}: columns in place {n}^2: {t(lambda: lct2d.columns_inplace(full, p, ws)):.3f} ms", flush=True)
 print(f"{tag}: 2-D {n}^2: {t(lambda: lct2d.lct2d(f, p, p, out=out, workspace=ws)):.3f} ms", flush=True)
+import hashlib  # noqa: E402
+
+lct2d.lct2d(f, p, p, out=out, workspace=ws)
+torch.cuda.synchronize()
+print(f"{tag}: 2-D output sha {hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()[:16]}", flush=True)

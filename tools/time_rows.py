@@ -10,6 +10,10 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _variant import use_variant  # noqa: E402
+
+VARIANT = use_variant()
 
 
 def main():
@@ -53,7 +57,10 @@ def main():
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) * 1e3 / a.reps)
     nbytes = sets[0][0].numel() * sets[0][0].element_size() * 2
-    print(json.dumps({"n": a.n, "rows": a.rows, "dtype": a.dtype, "us": round(best, 2),
+    import hashlib
+
+    sha = hashlib.sha256(sets[0][1].cpu().numpy().tobytes()).hexdigest()[:16]
+    print(json.dumps({"variant": VARIANT, "sha": sha, "n": a.n, "rows": a.rows, "dtype": a.dtype, "us": round(best, 2),
                       "GBps": round(nbytes / best / 1e3, 1)}), flush=True)
 
 
