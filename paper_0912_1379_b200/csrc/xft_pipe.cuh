@@ -37,8 +37,17 @@
 #ifndef XFT_NOMEM
 #define XFT_NOMEM 0  // tuning only: a CTA re-reads / rewrites its first tile (L2-resident: compute-bound timing)
 #endif
+// L2 bulk prefetch (cp.async.bulk.prefetch.L2) of the tile this many tiles beyond the TMA ring, issued when a
+// tile's transform starts, so the later TMA load is an L2 hit (PipeCfg::L2PF).  Measured per kernel, depth 1
+// against off (A/B on one box, outputs bit-identical): c128 n = 4096 116.7 -> 115.6 us, c64 n = 16384 (one CTA
+// per SM) 945 -> 900 us, c64 n = 1024 (config 4) 184.0 -> 178.3 us: on.  c64 n = 4096 / 8192 (single-stage CTAs
+// at 4 / 2 per SM) +1.3-1.5%, c128 n = 2048 +2%, c128 n = 8192 and the short-row rings: no change: off.
+// Depths 2 and 3 are slower everywhere (c128 n = 4096: 117.0 / 122.4 us).
+#ifndef XFT_L2PF_EARLY
+#define XFT_L2PF_EARLY 0  // 1: issue the prefetch before waiting for the current tile instead of after
+#endif
 #ifndef XFT_L2PF
-#define XFT_L2PF 0  // tiles of L2 bulk prefetch beyond the TMA ring (0 = off)
+#define XFT_L2PF -1  // >= 0: force this depth on every row kernel (tuning)
 #endif
 #ifndef XFT_C128_TABCOPIES
 #define XFT_C128_TABCOPIES 1
@@ -100,6 +109,10 @@
 #endif
 #ifndef XFT_XBAR128
 #define XFT_XBAR128 0     // c128 row kernels
+#endif
+
+#ifndef XFT_SPLIT4
+#define XFT_SPLIT4 0  // 1: the split next-row prefetch for c64 single-row CTAs at 2 and 4 CTAs per SM too (n = 8192, 4096)
 #endif
 
 #ifndef XFT_SKELETON
@@ -487,7 +500,8 @@ struct PipeCfg {
   static constexpr size_t SMEM_MAX = MINB_ == 1 ? 232448 - 8192  // 227 KB opt-in minus static shared memory
                                                 : 233472 / (MINB_ > 0 ? MINB_ : 1) - 1024 - STATIC_EST;
   static constexpr size_t MAIN = size_t(STAGES) * STAGE * sizeof(C) + TAB_BYTES;
-  static constexpr int SPLIT0 = (SPLITOK_ && ROWS == 1 && STAGES == 1 && (MINB_ == 1 || (MINB_ == 2 && XFT_SPLIT2)) &&
+  static constexpr int SPLIT0 = (SPLITOK_ && ROWS == 1 && STAGES == 1 &&
+                                 (MINB_ == 1 || (MINB_ == 2 && XFT_SPLIT2) || (!C128 && MINB_ > 1 && XFT_SPLIT4)) &&
                                  XFT_SPLIT && SMEM_MAX > MAIN)
                                     ? int((SMEM_MAX - MAIN) / sizeof(C)) / TR * TR : 0;
   static constexpr int SPLIT = SPLIT0 < N ? SPLIT0 : 0;
@@ -513,6 +527,10 @@ struct PipeCfg {
                   : SPLITOK_ && BARTH_ == 0 &&
                         (sizeof(C_) == 16 ? XFT_XBAR128 != 0 : (XFT_XBAR64_ALL || (XFT_XBAR64 && MINB_ == 1))));
   static constexpr bool XBAR_LAST = XBAR && XBAR_ < 0 && STAGES_ == 1;
+  // L2 prefetch depth of the row kernels (tiles beyond the ring; see XFT_L2PF_*)
+  static constexpr int L2PF = !SPLITOK_       ? 0
+                              : XFT_L2PF >= 0 ? XFT_L2PF
+                              : (sizeof(C_) == 16 ? LOG2N_ == 12 : (LOG2N_ == 14 || LOG2N_ == 10)) ? 1 : 0;
   static_assert(NPASS >= 2, "pipelined kernel needs at least one exchange");
   static_assert(TR >= 2, "k & 1 == j & 1 needs an even thread stride");
   static_assert(THREADS <= 1024, "threads");
@@ -1222,15 +1240,19 @@ xft_pipe_kernel(const typename Cfg::C* __restrict__ in, typename Cfg::C* __restr
         __syncthreads();
       }
     }
-    mbar_wait(&bars[st], (uint32_t)((it / S) & 1));
-    if constexpr (XFT_L2PF > 0) {
-      // pull the tile XFT_L2PF ahead of the ring into L2 while this one is transformed
-      const long long pt = tile + (long long)(S - 1 + XFT_L2PF) * G;
-      if (tid == 0 && pt < ntiles) {
-        const long long rows = batch - pt * ROWS < ROWS ? batch - pt * ROWS : ROWS;
-        tma_prefetch_l2(in + pt * Cfg::TILE, (uint32_t)(rows * N * sizeof(C)));
+    auto l2_prefetch = [&]() {
+      if constexpr (Cfg::L2PF > 0 && !XFT_NOMEM) {
+        // pull the tile L2PF ahead of the ring into L2 while this one is transformed
+        const long long pt = tile + (long long)(S - 1 + Cfg::L2PF) * G;
+        if (tid == 0 && pt < ntiles) {
+          const long long rows = batch - pt * ROWS < ROWS ? batch - pt * ROWS : ROWS;
+          tma_prefetch_l2(in + pt * Cfg::TILE, (uint32_t)(rows * N * sizeof(C)));
+        }
       }
-    }
+    };
+    if constexpr (XFT_L2PF_EARLY) l2_prefetch();
+    mbar_wait(&bars[st], (uint32_t)((it / S) & 1));
+    if constexpr (!XFT_L2PF_EARLY) l2_prefetch();
     C* const stg = stage0 + size_t(st) * Cfg::STAGE;
     const C* rs = stg + size_t(lrow) * N;      // this row's input (TMA layout)
     C* xs = stg + size_t(lrow) * Cfg::NP;      // this row's exchange buffer (read-after-barrier)
