@@ -121,7 +121,8 @@ int launch_blue(const void* in, void* out, long long rows, const int* rowlist, c
   } else {
     constexpr int dtype = sizeof(C) == 8 ? XFT_C64 : XFT_C128;
     constexpr int E = blue_radix(dtype, L);
-    using BC = BlueCfg<C, L, E>;
+    using BC = BlueStage<C, L, E, Op>;  // (SMEM: the exchange buffer + the Mehler apply CTAs' spectrum stage)
+    constexpr int TR = (1 << L) / E;
     auto kern = xft_blue_kernel<C, L, E, Op>;
     Tables tb;
     int rc = get_tables(int64_t(1) << L, dtype, &tb, E);
@@ -132,10 +133,10 @@ int launch_blue(const void* in, void* out, long long rows, const int* rowlist, c
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BC::TR, BC::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TR, BC::SMEM);
     const long long cap = (long long)sms * (occ < 1 ? 1 : (occ > 8 ? 8 : occ));  // Mehler scratch: <= 8 rows/SM
     const long long grid = rows < cap ? rows : cap;
-    kern<<<(unsigned)grid, BC::TR, BC::SMEM, st>>>(static_cast<const C*>(in), static_cast<C*>(out), rows, rowlist, op,
+    kern<<<(unsigned)grid, TR, BC::SMEM, st>>>(static_cast<const C*>(in), static_cast<C*>(out), rows, rowlist, op,
                                                    static_cast<const C*>(tb.tw));
     return cudaGetLastError() == cudaSuccess ? XFT_OK : XFT_ECUDA;
   }
