@@ -28,9 +28,6 @@ const long double PI_L = 3.141592653589793238462643383279502884L;
 
 constexpr int MAXL_C64 = 14;   // M <= 16384 (128 KiB exchange buffer)
 constexpr int MAXL_C128 = 13;  // M <= 8192
-#ifndef XFT_MEHLER_WAVES
-#define XFT_MEHLER_WAVES 1  // Mehler plans: balance the in-CTA size classes against the device's wave size (build_mehler_plan)
-#endif
 
 // iterative radix-2 FFT, sign s (plan-time only)
 void host_fft(std::vector<cld>& a, int s) {
@@ -117,10 +114,8 @@ int get_plan(int64_t n, int sign, int mode, CzPlan* out) {
   return XFT_OK;
 }
 
-// `wave` non-null: no launch, *wave = the CTAs resident at once (SMs x occupancy), i.e. the rows of one round
 template <class C, int L, class Op>
-int launch_blue(const void* in, void* out, long long rows, const int* rowlist, const Op& op, cudaStream_t st,
-                long long* wave = nullptr) {
+int launch_blue(const void* in, void* out, long long rows, const int* rowlist, const Op& op, cudaStream_t st) {
   if constexpr (L < 2) {
     return XFT_ENOTSUP;
   } else {
@@ -140,10 +135,6 @@ int launch_blue(const void* in, void* out, long long rows, const int* rowlist, c
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TR, BC::SMEM);
     const long long cap = (long long)sms * (occ < 1 ? 1 : (occ > 8 ? 8 : occ));  // Mehler scratch: <= 8 rows/SM
-    if (wave) {
-      *wave = cap;
-      return XFT_OK;
-    }
     const long long grid = rows < cap ? rows : cap;
     kern<<<(unsigned)grid, TR, BC::SMEM, st>>>(static_cast<const C*>(in), static_cast<C*>(out), rows, rowlist, op,
                                                    static_cast<const C*>(tb.tw));
@@ -153,9 +144,9 @@ int launch_blue(const void* in, void* out, long long rows, const int* rowlist, c
 
 template <class C, class Op, int... Ls>
 int dispatch_blue(int l, const void* in, void* out, long long rows, const int* rowlist, const Op& op,
-                  cudaStream_t st, std::integer_sequence<int, Ls...>, long long* wave = nullptr) {
+                  cudaStream_t st, std::integer_sequence<int, Ls...>) {
   int rc = XFT_ENOTSUP;
-  ((l == Ls ? (rc = launch_blue<C, Ls, Op>(in, out, rows, rowlist, op, st, wave), 0) : 0), ...);
+  ((l == Ls ? (rc = launch_blue<C, Ls, Op>(in, out, rows, rowlist, op, st), 0) : 0), ...);
   return rc;
 }
 
@@ -164,16 +155,6 @@ int blue(int l, const void* in, void* out, long long rows, const int* rowlist, c
   constexpr int MAXL = sizeof(C) == 8 ? MAXL_C64 : MAXL_C128;
   if (l < 2 || l > MAXL) return XFT_ENOTSUP;
   return dispatch_blue<C, Op>(l, in, out, rows, rowlist, op, st, std::make_integer_sequence<int, MAXL + 1>{});
-}
-
-// rows one round of the in-CTA Mehler apply kernel of size class l holds on the current device (0: not an in-CTA class)
-long long mehler_wave(int l) {
-  long long wave = 0;
-  if (l < 2 || l > MAXL_C128) return 0;
-  if (dispatch_blue<double2, OpMehler>(l, nullptr, nullptr, 0, nullptr, OpMehler{}, nullptr,
-                                       std::make_integer_sequence<int, MAXL_C128 + 1>{}, &wave) != XFT_OK)
-    return 0;
-  return wave;
 }
 
 int log2_ceil(int64_t v) {
@@ -399,36 +380,6 @@ int build_mehler_plan(int dev, int64_t batch, int64_t n, std::vector<double> zv,
     rows[r] = pr.p;
     classes[pr.l].push_back((int)r);
   }
-#if XFT_MEHLER_WAVES
-  // Wave balancing.  An in-CTA class of R rows runs ceil(R / wave) rounds of `wave` rows (SMs x resident CTAs,
-  // one row per CTA and round).  When the last round would be nearly empty (R mod wave <= wave / 8: config 3
-  // has 598 rows of M = 8192 for 148 one-CTA SMs, i.e. a fifth round of 6 rows, 20% of that kernel's time),
-  // its rows -- the widest windows of the class -- move up one size class (a longer convolution holds the same
-  // window; only the 1/M in `scale` changes), where they cost a fraction of the round they free.
-  {
-    const int lmax = log2_ceil(2 * n - 1);  // the largest class a row of this n can land in by itself
-    for (int l = 2; l <= MAXL_C128 && l < lmax; ++l) {
-      auto it = classes.find(l);
-      if (it == classes.end()) continue;
-      const long long wave = mehler_wave(l), R = (long long)it->second.size();
-      if (wave <= 0 || R <= wave) continue;
-      const long long extra = R % wave;
-      if (extra == 0 || extra > wave / 8) continue;
-      std::vector<int>& v = it->second;
-      std::stable_sort(v.begin(), v.end(), [&](int a, int b) { return rows[a].wn < rows[b].wn; });
-      std::vector<int>& up = classes[l + 1];
-      for (long long i = 0; i < extra; ++i) {
-        const int r = v.back();
-        v.pop_back();
-        rows[r].scale.x *= 0.5;  // 1/M of the doubled convolution length (exact)
-        rows[r].scale.y *= 0.5;
-        up.push_back(r);
-      }
-      std::sort(v.begin(), v.end());
-      std::sort(up.begin(), up.end());
-    }
-  }
-#endif
   std::vector<int> list;
   list.reserve(batch);
   for (auto& kv : classes) {
