@@ -82,8 +82,12 @@
 #ifndef XFT_RING_PERSIST_MB
 #define XFT_RING_PERSIST_MB 0  // > 0: set the device's persisting-L2 set-aside once (48: the ring stops leaking to HBM,
 #endif                         // 2.9 -> 2.1 GB written, but the kernel slows 1.26 -> 1.40 ms: less L2 for the streams)
+#ifndef XFT_RING_PF
+#define XFT_RING_PF 0      // > 0: the issuer pulls the pass-1 input tiles of its next XFT_RING_PF decoded-but-unissued
+#endif                     // tiles into L2 (bulk tensor prefetch).  A/B, 16384^2: 1.311 (1), 1.32 (2) vs 1.257 ms: off
 #ifndef XFT_RING_XBAR
 #define XFT_RING_XBAR 0    // 1: the "tile has been read" barrier of the compute warps is a split mbarrier phase
+                           // (PipeCfg::XBAR).  A/B, 16384^2: 1.272 vs 1.257 ms: off
 #endif
 #ifndef XFT_RING_HINT
 #define XFT_RING_HINT 1    // L2 eviction hints: input evict_first, scratch evict_last
@@ -358,6 +362,7 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
     const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
     // tickets fetched; dependencies verified; tiles issued (incl. the end marker); stage releases observed
     int nf = 0, nd = 0, ni = 0, nrel = 0;
+    int npf = 0;  // XFT_RING_PF: tiles whose input has been prefetched into L2 (or skipped)
     bool ended = false;
     const unsigned* ok_ctr = nullptr;  // the last dependency counter seen complete
     unsigned long long idle_since = 0;
@@ -393,6 +398,15 @@ xft_colring_kernel(const __grid_constant__ CUtensorMap map, float2* __restrict__
           ok_ctr = ctr;
           fence_proxy_async_all();  // the acquired generic-proxy stores (scratch) are read by bulk copies
           ++nd;
+          progress = true;
+        }
+      }
+      if constexpr (XFT_RING_PF > 0) {
+        if (npf < ni) npf = ni;  // already issued: nothing to prefetch
+        if (npf < nf && npf < ni + XFT_RING_PF) {
+          const RingTile tp = info[npf % NI];
+          if (tp.phase == 0) tma_prefetch_3d(&map, tp.cb * W, tp.idx, 0);
+          ++npf;
           progress = true;
         }
       }
