@@ -101,6 +101,10 @@
 // one-CTA-per-SM c64 row kernel (n = 16384) 1016 -> 951 us; with 2 or 4 CTAs per SM, where the other CTAs already
 // fill a CTA-wide rendezvous, it LOSES: config 2 c64 52.8 -> 58.3 us, c128 117.4 -> 126.5 us (n = 8192: 296 ->
 // 335 us), config 4 184.9 -> 188.2 us.  Hence: c64 at one CTA per SM only.
+// Two follow-ups, both measured slower and removed: replacing only the row's last rendezvous (thread 0 waits on an
+// mbarrier phase, the other warps go on) at 2-4 CTAs per SM -- c64 52.7 -> 57.1 us, c128 115.6 -> 120.8 us; and
+// letting the warp that arrives last hand the stage back to the TMA instead of thread 0 waiting for the phase --
+// n = 16384: 900 -> 948 us (the slowest warp gets the extra work).
 #ifndef XFT_XBAR64
 #define XFT_XBAR64 1      // c64 row kernels at one CTA per SM
 #endif
