@@ -63,3 +63,31 @@ def test_random_dft_rows(torch, k):
     ref = O.dft_rows(f.astype(np.complex128), sign)
     tol = 1e-12 if dtype == np.complex128 else 2e-5
     assert max_row_rel_l2(got.astype(np.complex128), ref) <= tol, (n, dtype.__name__)
+
+
+# Batch sizes around the persistent grids of the row kernels that use split "buffer read" barriers and the
+# L2 prefetch (c64 n = 16384: one CTA per SM; c128 n = 4096: two; c64 n = 1024: 8-row tiles): fewer rows than
+# CTAs, one row more than a full round, ragged last tiles.  A row's result must not depend on the batch it is
+# in (bitwise), must repeat bitwise, and must match the oracle.
+@pytest.mark.parametrize("n,dtype,rows", [
+    (16384, np.complex64, 1), (16384, np.complex64, 149), (16384, np.complex64, 300),
+    (4096, np.complex128, 297), (4096, np.complex128, 593), (1024, np.complex64, 2371),
+])
+def test_persistent_grid_edges(torch, n, dtype, rows):
+    from paper_0912_1379_b200 import ops
+
+    rng = np.random.default_rng(n + rows)
+    al = rng.uniform(0.05, np.pi - 0.05, rows)
+    abcd = np.stack([np.cos(al), np.sin(al), -np.sin(al), np.cos(al)], 1)
+    f = ((rng.standard_normal((rows, n)) + 1j * rng.standard_normal((rows, n))) / math.sqrt(2)).astype(dtype)
+    v = torch.from_numpy(f).cuda()
+    got = ops.lct_rows(v, abcd).cpu().numpy()
+    again = ops.lct_rows(v, abcd).cpu().numpy()
+    assert np.array_equal(got, again)
+    pick = sorted({0, rows - 1, rows // 2, min(rows - 1, 148), min(rows - 1, 296)})
+    for r in pick:  # the same row alone: another grid, another tile position
+        alone = ops.lct_rows(v[r:r + 1].clone(), abcd[r:r + 1]).cpu().numpy()
+        assert np.array_equal(alone[0], got[r]), (n, rows, r)
+    _, ref = O.fast_lct_rows(abcd[pick], f[pick].astype(np.complex128))
+    tol = 1e-12 if dtype == np.complex128 else 2e-5
+    assert max_row_rel_l2(got[pick].astype(np.complex128), ref) <= tol
