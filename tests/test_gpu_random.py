@@ -82,8 +82,9 @@ def test_persistent_grid_edges(torch, n, dtype, rows):
     f = ((rng.standard_normal((rows, n)) + 1j * rng.standard_normal((rows, n))) / math.sqrt(2)).astype(dtype)
     v = torch.from_numpy(f).cuda()
     got = ops.lct_rows(v, abcd).cpu().numpy()
-    again = ops.lct_rows(v, abcd).cpu().numpy()
-    assert np.array_equal(got, again)
+    for _ in range(6 if n == 16384 else 2):  # (the split-barrier kernel: a shared-memory race would show up as jitter)
+        again = ops.lct_rows(v, abcd).cpu().numpy()
+        assert np.array_equal(got, again)
     pick = sorted({0, rows - 1, rows // 2, min(rows - 1, 148), min(rows - 1, 296)})
     for r in pick:  # the same row alone: another grid, another tile position
         alone = ops.lct_rows(v[r:r + 1].clone(), abcd[r:r + 1]).cpu().numpy()
