@@ -1,6 +1,6 @@
 #!/bin/bash
-# build_variant_large.sh NAME "-DFLAGS..." : tune/libxft_NAME.so = the default objects (csrc/build, `make` first)
-# with xft_bluestein.cu alone rebuilt under the flags (column-kernel tuning only)
+# build_variant_blue.sh NAME "-DFLAGS..." : tune/libxft_NAME.so = the default objects (csrc/build, `make` first)
+# with xft_bluestein.cu alone rebuilt under the flags (chirp-z / Mehler kernel tuning only)
 set -e
 cd "$(dirname "$0")/../paper_0912_1379_b200/csrc"
 mkdir -p ../../tune

@@ -1,6 +1,6 @@
 #!/bin/bash
-# build_variant_large.sh NAME "-DFLAGS..." : tune/libxft_NAME.so = the default objects (csrc/build, `make` first)
-# with xft_capi.cu alone rebuilt under the flags (column-kernel tuning only)
+# build_variant_capi.sh NAME "-DFLAGS..." : tune/libxft_NAME.so = the default objects (csrc/build, `make` first)
+# with xft_capi.cu alone rebuilt under the flags (row-kernel tuning only)
 set -e
 cd "$(dirname "$0")/../paper_0912_1379_b200/csrc"
 mkdir -p ../../tune
