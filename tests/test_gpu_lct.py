@@ -126,17 +126,17 @@ def test_config4_rows_golden(torch, X, golden):
 
 @pytest.mark.parametrize("dtype,tol", [(np.complex64, TOL64), (np.complex128, TOL128)])
 def test_config2_full_batch(torch, X, dtype, tol):
-    """Full 4096 x 4096 batch: oracle on sampled rows (incl. the extreme-phase rows) + norm identity on all rows."""
+    """Full 4096 x 4096 batch: EVERY row against the oracle (chunked) + the norm identity on all rows."""
     from paper_0912_1379_b200 import workloads
 
     c2 = workloads.config2(dtype=dtype)
     got_t = X.ops.lct_rows(dev(torch, c2.values), c2.abcd)
-    alpha = c2.extra["alpha"]
-    rows = sorted(set([0, 1, 2, 4095, int(np.argmin(alpha)), int(np.argmax(alpha)),
-                       int(np.argmin(np.abs(alpha - math.pi / 2)))] + list(range(100, 4096, 397))))
-    got = got_t[rows].cpu().numpy()
-    _, ref = O.fast_lct_rows(c2.abcd[rows], c2.values[rows].astype(np.complex128))
-    assert max_row_rel_l2(got, ref) <= tol
+    got_all = got_t.cpu().numpy()
+    worst = 0.0
+    for r0 in range(0, c2.values.shape[0], 512):
+        _, ref = O.fast_lct_rows(c2.abcd[r0:r0 + 512], c2.values[r0:r0 + 512].astype(np.complex128))
+        worst = max(worst, max_row_rel_l2(got_all[r0:r0 + 512], ref))
+    assert worst <= tol, worst
     # ||G||^2 = pi/(4|b|) ||f||^2 on every row (SURVEY 8(a))
     f = dev(torch, c2.values).to(torch.complex128)
     lhs = (got_t.to(torch.complex128).abs() ** 2).sum(dim=1).cpu().numpy()
@@ -172,10 +172,14 @@ def test_config4_full_batch_and_quadrature(torch, X):
 
     c4 = workloads.config4()
     got_t = X.ops.lct_rows(dev(torch, c4.values), c4.abcd)
+    got_all = got_t.cpu().numpy()
+    worst = 0.0
+    for r0 in range(0, c4.values.shape[0], 8192):  # every one of the 65536 rows against the oracle
+        _, ref = O.fast_lct_rows(c4.abcd, c4.values[r0:r0 + 8192].astype(np.complex128))
+        worst = max(worst, max_row_rel_l2(got_all[r0:r0 + 8192], ref))
+    assert worst <= TOL64, worst
     rows = [0, 1, 777, 65535]
-    got = got_t[rows].cpu().numpy()
-    _, ref = O.fast_lct_rows(c4.abcd, c4.values[rows].astype(np.complex128))
-    assert max_row_rel_l2(got, ref) <= TOL64
+    got = got_all[rows]
     # the continuous transform of the Hermite-Gaussian mixture (quadrature error report)
     cf = workloads.config4_closed_form(c4.extra["coeffs"][rows])
     lo, hi = 1024 // 10, 9 * 1024 // 10
