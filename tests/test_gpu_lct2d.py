@@ -286,6 +286,41 @@ def test_config5_256_rows_and_256_columns_independent(torch, L2):
         assert rel_l2(out[c, :], want_rows[i]) <= 2e-5, ("row", c)
 
 
+def test_config5_every_element_two_routes(torch, L2):
+    """Config 5 at full size, every one of the 2^28 outputs: the 2-D transform (row kernel, then the L2-staged
+    column kernel) against the same transform done with the row kernel alone on both axes (rows, transpose,
+    rows, transpose) -- the 1-D row kernel is what the golden vectors, the full config-2/4 batches and the
+    random sweep pin to the oracle.  Two independent c64 roundings: per-column relative L2 <= 2e-5."""
+    from paper_0912_1379_b200 import ops, workloads
+
+    n = 16384
+    ft = torch.from_numpy(workloads.config5_field(n)).cuda()
+    out = L2.lct2d(ft, ABCD5, ABCD5)
+    rows = ops.lct_rows(ft, ABCD5)
+    # 512 rows of the row pass, and below 512 of the transposed pass, against the oracle itself
+    pick = np.unique(np.concatenate([[0, n // 2, n - 1], np.random.default_rng(5).choice(n, 509, replace=False)]))
+    _, want = O.fast_lct_rows(ABCD5, ft[pick].cpu().numpy().astype(np.complex128))
+    got = rows[pick].cpu().numpy()
+    assert max(rel_l2(got[i], want[i]) for i in range(len(pick))) <= 2e-5
+    del ft
+    rt = rows.T.contiguous()
+    del rows
+    ref_t = ops.lct_rows(rt, ABCD5)  # [column, row]: the column LCTs as rows of the transposed field
+    _, want = O.fast_lct_rows(ABCD5, rt[pick].cpu().numpy().astype(np.complex128))
+    got = ref_t[pick].cpu().numpy()
+    assert max(rel_l2(got[i], want[i]) for i in range(len(pick))) <= 2e-5
+    del rt
+    num = torch.zeros(n, dtype=torch.float64, device="cuda")
+    den = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for c0 in range(0, n, 2048):  # per output column, in slabs (bounded temporaries)
+        a = out[:, c0:c0 + 2048].to(torch.complex128)
+        b = ref_t[c0:c0 + 2048, :].T.to(torch.complex128)
+        num[c0:c0 + 2048] = ((a - b).abs() ** 2).sum(dim=0)
+        den[c0:c0 + 2048] = (b.abs() ** 2).sum(dim=0)
+    err = float(torch.sqrt(num / den).max())
+    assert err <= 2e-5, err
+
+
 @pytest.mark.parametrize("nc,ld", [(64, 64), (65, 66), (200, 256), (1000, 1024)])
 def test_ring_columns_ragged_and_repeatable(torch, L2, nc, ld):
     """The L2-staged column kernel (16384 rows, c64) on ragged slabs: partial last 64-column block, row
